@@ -1,0 +1,25 @@
+"""Shared pytest configuration.
+
+Markers: `gpu` = needs a B200 (run on the GPU box with `-m gpu`); everything
+else runs on the CPU-only build container (`-m "not gpu"`).
+"""
+
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN = ROOT / "tests" / "golden"
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+@pytest.fixture(scope="session")
+def golden_dir():
+    return GOLDEN
