@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark: decoded coded Gbit/s of batched layered min-sum on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+BASELINE.json metric: "decoded coded Gbit/s per GPU and at 1/2/4/8 B200 (fixed
+iters); % of roofline".  Default workload = BASELINE configs[1] (C2: WiMAX
+N=2304 R=1/2, float32, 10 fixed iterations, 65536 codewords per GPU,
+BPSK/AWGN at 1.5 dB).  A step = one decode pass over the whole batch.
+
+`value`  device-resident decode throughput: inputs already in HBM, one
+         libqcb200 launch per step, CUDA events on the launching stream,
+         barrier + synchronize around the K timed steps, max over ranks;
+         Gbit/s = ranks * W * N / time.  Inputs (604 MB for C2) exceed the
+         126 MB L2, so no explicit flush is needed between steps.
+`e2e`    the same decode through the reference-facing C ABI drop-in
+         (`qc_decode_batch_f32_host`, i.e. `_kernels.decode_batch_f32`) with
+         pinned host buffers: H2D of the LLRs, decode, D2H of hard bits /
+         iterations / convergence flags inside every timed step.
+`roofline` the decoder is ALU-issue bound: 12 lane-ops per
+         edge-update, peak = SMs x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json).
+`cpu_baseline` the CPU oracle port (oracle/qc_oracle.c, the reference's
+         decode loops restated in C, one pthread per host core) timed on a
+         bounded sample of the same workload on rank 0 at N=1.
+
+Multi-GPU (torchrun, one rank per GPU): each rank decodes its own W codewords
+(weak scaling, no data-path collective); the per-rank error/iteration
+counters are summed with one NCCL all_reduce after the timed region.
+
+`--impl reference` times the reference's CPU decode (the oracle port, all
+host threads) on the same config/metric on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+OPS_PER_EDGE_UPDATE = 12   # SURVEY.md §8d algorithmic ALU ops per edge-update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def ncu_traffic(config: str):
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if any."""
+    for f in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+            if config in d and d[config].get("dram_bytes_per_launch"):
+                return d[config]["dram_bytes_per_launch"], f.name
+        except Exception:
+            continue
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def coded_bits(wl):
+    from paper_2306_12063_b200 import codebook as CB
+    return sum(CB.get_model_matrix(*c).n for c in wl.codes) * wl.w_per_code
+
+
+def edge_updates(wl):
+    from paper_2306_12063_b200 import codebook as CB
+    return sum(CB.get_model_matrix(*c).edges for c in wl.codes) * wl.w_per_code * wl.iters
+
+
+def hbm_bytes(wl):
+    """Algorithmic HBM bytes per step: LLR in + unpacked hard bits out + iters/conv."""
+    from paper_2306_12063_b200 import codebook as CB
+    b = 2 if wl.fixed else 4
+    return sum(CB.get_model_matrix(*c).n * (b + 1) + 5 for c in wl.codes) * wl.w_per_code
+
+
+# --- CPU (oracle port) -----------------------------------------------------------
+
+def cpu_decode_rate(wl, seconds: float, threads: int):
+    """Coded Gbit/s of the oracle port on a bounded sample of the workload."""
+    from oracle import oracle as O
+    from paper_2306_12063_b200 import codebook as CB
+    from paper_2306_12063_b200.workloads import host_llrs
+    rates, sample_desc = [], []
+    per_code = max(1.0, seconds / len(wl.codes))
+    total_bits = total_t = 0.0
+    for ci, code in enumerate(wl.codes):
+        mm = CB.get_model_matrix(*code)
+        h = CB.expand(mm)
+        w = max(threads * 2, 64)
+        llr, _ = host_llrs(mm, w, wl.ebn0_db, [wl.seed, ci, 99], wl.fixed)
+        t0 = time.perf_counter()
+        O.decode_batch(h, llr, wl.iters, False, workers=threads)
+        dt = time.perf_counter() - t0
+        w2 = int(min(max(w, w * per_code / max(dt, 1e-6)), 1 << 17))
+        w2 = max(threads, (w2 // threads) * threads)
+        llr, _ = host_llrs(mm, w2, wl.ebn0_db, [wl.seed, ci, 100], wl.fixed)
+        t0 = time.perf_counter()
+        O.decode_batch(h, llr, wl.iters, False, workers=threads)
+        dt = time.perf_counter() - t0
+        total_bits += w2 * mm.n
+        total_t += dt
+        sample_desc.append(f"{code[0]} {code[1]} {code[2]}: {w2} cw in {dt:.2f} s")
+        rates.append(w2 * mm.n / dt / 1e9)
+    return total_bits / total_t / 1e9, "; ".join(sample_desc)
+
+
+def run_reference(args, wl):
+    rank, _, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+    from paper_2306_12063_b200 import codebook as CB
+    from paper_2306_12063_b200.workloads import host_llrs
+    # each step = a bounded sample of the workload (one chunk per code)
+    mms = [CB.get_model_matrix(*c) for c in wl.codes]
+    per_step = max(threads * 2, 256 // len(mms))
+    inputs = []
+    for ci, mm in enumerate(mms):
+        llr, _ = host_llrs(mm, per_step, wl.ebn0_db, [wl.seed, ci, 7], wl.fixed)
+        inputs.append((CB.expand(mm), llr, mm.n))
+    for _ in range(args.warmup):
+        for h, llr, _ in inputs:
+            O.decode_batch(h, llr, wl.iters, False, workers=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for h, llr, _ in inputs:
+            O.decode_batch(h, llr, wl.iters, False, workers=threads)
+        times.append(time.perf_counter() - t0)
+    bits = sum(llr.shape[0] * n for _, llr, n in inputs)
+    t = sum(times)
+    value = bits * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": f"decoded coded Gbit/s ({wl.key}, fixed {wl.iters} iters)",
+        "value": round(value, 6), "unit": "Gbit/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int16" if wl.fixed else "f32", "data": "synthetic (seeded BPSK/AWGN, reference recipe)",
+        "config": config_dict(wl, args),
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} codewords per code per step, {len(mms)} code(s); "
+                                   "oracle/qc_oracle.c = reference _kernels.py loops in C, one pthread per core"},
+        "e2e": {"value": round(value, 6), "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def config_dict(wl, args):
+    from paper_2306_12063_b200 import codebook as CB
+    names = [f"{c[0]}-{c[1]}-r{c[2].replace('/', '')}" for c in wl.codes]
+    return {"workload": f"{wl.key}: " + (names[0] if len(names) == 1 else f"{len(names)} codes mixed"),
+            "codewords_per_gpu": wl.w_total, "n_bits": CB.get_model_matrix(*wl.codes[0]).n,
+            "iterations": wl.iters, "early_termination": False, "ebn0_db": wl.ebn0_db,
+            "arithmetic": wl.arithmetic.value, "parallelism": f"dp{args.gpus} (codeword shards)",
+            "l2": "inputs larger than L2 (no flush needed)" if hbm_bytes(wl) > 126e6 else
+                  "inputs smaller than L2: L2 flushed between steps"}
+
+
+# --- GPU arm -----------------------------------------------------------------------
+
+def run_ours(args, wl):
+    import torch
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+    import paper_2306_12063_b200 as P
+    from paper_2306_12063_b200 import _lib
+    from paper_2306_12063_b200.workloads import device_llrs
+    _lib.lib()
+    cfg = wl.config()
+    mms = wl.model_matrices()
+    codes = [P.code_handle(mm) for mm in mms]
+    assert all(c.specialised for c in codes)
+    llrs, pools = [], []
+    for ci, mm in enumerate(mms):
+        t, pool = device_llrs(mm, wl.w_per_code, wl.ebn0_db, seed=wl.seed * 1000 + 10 * rank + ci,
+                              fixed=wl.fixed, device=dev)
+        llrs.append(t)
+        pools.append(pool)
+    outs = []
+    for mm, t in zip(mms, llrs):
+        w = t.shape[0]
+        outs.append((torch.empty((w, mm.n), dtype=torch.uint8, device=dev),
+                     torch.empty(w, dtype=torch.int32, device=dev),
+                     torch.empty(w, dtype=torch.uint8, device=dev)))
+    flush = None
+    if hbm_bytes(wl) <= 126e6:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+
+    def step():
+        for c, t, o in zip(codes, llrs, outs):
+            P.decode_batch(c, t, cfg, out=o, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize(dev)
+    # per-step events on the launching stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for i in range(args.steps):
+                if flush is not None:
+                    flush.zero_()
+                kev[i][0].record(stream)
+                step()
+                kev[i][1].record(stream)
+            ev[-1].record(stream)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    kernel_ms = [a.elapsed_time(b) for a, b in kev]
+    elapsed_ms = sum(kernel_ms)
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t_max.item())
+    ms_per_step = elapsed_ms / args.steps
+    bits_per_step = coded_bits(wl) * world
+    value = bits_per_step / (ms_per_step * 1e-3) / 1e9
+
+    # counters (bit/frame errors vs the transmitted codewords, iterations) -> one NCCL all_reduce
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    for (hard, iters, conv), pool, mm in zip(outs, pools, mms):
+        w = hard.shape[0]
+        ref = pool[torch.arange(w, device=dev) % pool.shape[0]]
+        err = (hard[:, :mm.k] != ref[:, :mm.k]).sum(dim=1)
+        cnt += torch.stack([err.sum(), (err > 0).sum(), iters.sum().to(torch.int64),
+                            conv.sum().to(torch.int64)])
+    if dist:
+        dist.all_reduce(cnt)
+    cnt = cnt.cpu().tolist()
+
+    peaks, peak_kind = measured_peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    kavg = statistics.mean(kernel_ms) * 1e-3
+    achieved = edge_updates(wl) * OPS_PER_EDGE_UPDATE / kavg / 1e12
+    traffic, traffic_src = ncu_traffic(wl.key)
+    hbm_ach = hbm_bytes(wl) / kavg / 1e9
+
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = run_e2e(args, wl, mms, llrs, world, dist, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        threads = os.cpu_count() or 1
+        v, sample = cpu_decode_rate(wl, args.cpu_seconds, threads)
+        cpu = {"value": round(v, 6), "unit": "Gbit/s", "cores": threads, "kind": "port",
+               "sample": sample + " (oracle/qc_oracle.c, reference _kernels.py loops in C)"}
+
+    if rank == 0:
+        line = {
+            "metric": f"decoded coded Gbit/s ({wl.key}, fixed {wl.iters} iters)",
+            "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int16" if wl.fixed else "f32",
+            "data": "synthetic (seeded BPSK/AWGN LLRs, reference channel recipe)",
+            "config": config_dict(wl, args),
+            "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(alu_peak, 3),
+                         "unit": "Tops/s", "frac": round(achieved / alu_peak, 4),
+                         "traffic": traffic,
+                         "note": f"{OPS_PER_EDGE_UPDATE} lane-ops per edge-update x {edge_updates(wl)} "
+                                 f"edge-updates per launch / avg launch {kavg * 1e3:.3f} ms; peak = {sms} SMs x 128 "
+                                 f"lanes x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz ({peak_kind} sm_max_mhz)"
+                                 + (f"; traffic from {traffic_src}" if traffic_src else ""),
+                         "hbm": {"achieved": round(hbm_ach, 1), "peak": peaks.get("hbm_gbs"),
+                                 "unit": "GB/s", "frac": round(hbm_ach / peaks.get("hbm_gbs", 6650.0), 4)}},
+            "gpu_launches": args.steps * len(codes),
+            "clocks": clocks.summary(),
+            "counters": {"bit_errors": cnt[0], "frame_errors": cnt[1], "iter_sum": cnt[2],
+                         "converged": cnt[3], "frames": wl.w_total * world,
+                         "ber": cnt[0] / max(1, wl.w_total * world * mms[0].k)},
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, wl, mms, llrs, world, dist, dev):
+    """The reference-facing drop-in (_kernels.decode_batch_*), pinned host buffers."""
+    import torch
+    from paper_2306_12063_b200 import _kernels
+    from paper_2306_12063_b200 import codebook as CB
+    steps = args.e2e_steps or max(3, min(args.steps, 10))
+    host = []
+    for mm, t in zip(mms, llrs):
+        h = CB.expand(mm)
+        src = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        src.copy_(t)
+        w = t.shape[0]
+        hard = torch.empty((w, mm.n), dtype=torch.uint8, pin_memory=True)
+        iters = torch.empty(w, dtype=torch.int32, pin_memory=True)
+        conv = torch.empty(w, dtype=torch.uint8, pin_memory=True)
+        host.append((h, src.numpy(), hard.numpy(), iters.numpy(), conv.numpy(), (src, hard, iters, conv)))
+    fn = _kernels.decode_batch_i16 if wl.fixed else _kernels.decode_batch_f32
+
+    def step():
+        for h, src, hard, iters, conv, _ in host:
+            fn(h.row_ptr, h.row_cols, h.m // h.z, h.z, src, wl.iters, 0, hard, iters, conv)
+
+    step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    b = 2 if wl.fixed else 4
+    h2d = sum(mm.n * b for mm in mms) * wl.w_per_code
+    d2h = sum(mm.n + 5 for mm in mms) * wl.w_per_code
+    return {"value": round(coded_bits(wl) * world * steps / dt / 1e9, 4), "unit": "Gbit/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "ms_per_step": round(dt * 1e3 / steps, 3),
+            "path": "_kernels.decode_batch_%s -> qc_decode_batch_%s_host (pinned host buffers)"
+                    % (("i16",) * 2 if wl.fixed else ("f32",) * 2)}
+
+
+def main():
+    args = parse()
+    if args.steps < 1 or args.warmup < 0:
+        raise SystemExit("steps >= 1, warmup >= 0")
+    from paper_2306_12063_b200.workloads import WORKLOADS
+    wl = WORKLOADS[args.config]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,29 +66,38 @@ static void decode_f32_range(const job_t *J, int64_t w0, int64_t w1) {
             for (int32_t t = 0; t < MB; ++t) {
                 for (int32_t m = t * Z; m < (t + 1) * Z; ++m) {
                     const int32_t lo = rp[m], deg = rp[m + 1] - lo;
+                    const int32_t *cols = ci + lo;
                     const float m1 = min1[m], m2 = min2[m];
                     const int32_t am = amin[m];
-                    const int64_t sb = sbits[m], sp = sprod[m];
+                    /* sign of L_old_j = sp ^ bit j of sb (:63) */
+                    const uint32_t sbx = sbits[m] ^ (sprod[m] ? 0xFFFFFFFFu : 0u);
                     float nm1 = INFINITY, nm2 = INFINITY;
                     int32_t nam = 0;
-                    int64_t nsb = 0, nsp = 0;
+                    uint32_t nsb = 0, nsp = 0;
                     for (int32_t j = 0; j < deg; ++j) {               /* :61-75 */
                         const float mag = (j == am) ? m2 : m1;
-                        const float lold = ((sp ^ ((sb >> j) & 1)) == 1) ? -mag : mag;
-                        const float zz = post[ci[lo + j]] - lold;
+                        const float lold = ((sbx >> j) & 1u) ? -mag : mag;
+                        const float zz = post[cols[j]] - lold;
                         zrow[j] = zz;
                         const float a = fabsf(zz);
-                        if (a < nm1) { nm2 = nm1; nm1 = a; nam = j; }
-                        else if (a < nm2) { nm2 = a; }
-                        if (zz < 0.0f) { nsb |= (int64_t)1 << j; nsp ^= 1; }
+                        /* if a < nm1: nm2 = nm1, nm1 = a, nam = j; elif a < nm2: nm2 = a
+                         * (written branch-free; same selections, NaN compares false) */
+                        const int lt1 = a < nm1, lt2 = a < nm2;
+                        nm2 = lt1 ? nm1 : (lt2 ? a : nm2);
+                        nm1 = lt1 ? a : nm1;
+                        nam = lt1 ? j : nam;
+                        const uint32_t neg = zz < 0.0f;
+                        nsb |= neg << j;
+                        nsp ^= neg;
                     }
+                    const uint32_t nsbx = nsb ^ (nsp ? 0xFFFFFFFFu : 0u);
                     for (int32_t j = 0; j < deg; ++j) {               /* :76-79 */
                         const float mag = (j == nam) ? nm2 : nm1;
-                        const float lnew = ((nsp ^ ((nsb >> j) & 1)) == 1) ? -mag : mag;
-                        post[ci[lo + j]] = zrow[j] + lnew;
+                        const float lnew = ((nsbx >> j) & 1u) ? -mag : mag;
+                        post[cols[j]] = zrow[j] + lnew;
                     }
                     min1[m] = nm1; min2[m] = nm2; amin[m] = (int8_t)nam;
-                    sbits[m] = (uint32_t)nsb; sprod[m] = (uint8_t)nsp;
+                    sbits[m] = nsb; sprod[m] = (uint8_t)nsp;
                 }
             }
             it = k + 1;                                               /* :85-96 */
@@ -130,29 +139,35 @@ static void decode_i16_range(const job_t *J, int64_t w0, int64_t w1) {
             for (int32_t t = 0; t < MB; ++t) {
                 for (int32_t m = t * Z; m < (t + 1) * Z; ++m) {
                     const int32_t lo = rp[m], deg = rp[m + 1] - lo;
+                    const int32_t *cols = ci + lo;
                     const int16_t m1 = min1[m], m2 = min2[m];
                     const int32_t am = amin[m];
-                    const int64_t sb = sbits[m], sp = sprod[m];
+                    const uint32_t sbx = sbits[m] ^ (sprod[m] ? 0xFFFFFFFFu : 0u);
                     int16_t nm1 = 32767, nm2 = 32767;                 /* :142-143 */
                     int32_t nam = 0;
-                    int64_t nsb = 0, nsp = 0;
+                    uint32_t nsb = 0, nsp = 0;
                     for (int32_t j = 0; j < deg; ++j) {               /* :147-161 */
                         const int16_t mag = (j == am) ? m2 : m1;
-                        const int16_t lold = ((sp ^ ((sb >> j) & 1)) == 1) ? w16(-(int32_t)mag) : mag;
-                        const int16_t zz = w16((int32_t)post[ci[lo + j]] - lold);
+                        const int16_t lold = ((sbx >> j) & 1u) ? w16(-(int32_t)mag) : mag;
+                        const int16_t zz = w16((int32_t)post[cols[j]] - lold);
                         zrow[j] = zz;
                         const int16_t a = w16(zz < 0 ? -(int32_t)zz : zz);  /* abs(-32768) stays -32768 */
-                        if (a < nm1) { nm2 = nm1; nm1 = a; nam = j; }
-                        else if (a < nm2) { nm2 = a; }
-                        if (zz < 0) { nsb |= (int64_t)1 << j; nsp ^= 1; }
+                        const int lt1 = a < nm1, lt2 = a < nm2;
+                        nm2 = lt1 ? nm1 : (lt2 ? a : nm2);
+                        nm1 = lt1 ? a : nm1;
+                        nam = lt1 ? j : nam;
+                        const uint32_t neg = zz < 0;
+                        nsb |= neg << j;
+                        nsp ^= neg;
                     }
+                    const uint32_t nsbx = nsb ^ (nsp ? 0xFFFFFFFFu : 0u);
                     for (int32_t j = 0; j < deg; ++j) {               /* :162-165 */
                         const int16_t mag = (j == nam) ? nm2 : nm1;
-                        const int16_t lnew = ((nsp ^ ((nsb >> j) & 1)) == 1) ? w16(-(int32_t)mag) : mag;
-                        post[ci[lo + j]] = w16((int32_t)zrow[j] + lnew);
+                        const int16_t lnew = ((nsbx >> j) & 1u) ? w16(-(int32_t)mag) : mag;
+                        post[cols[j]] = w16((int32_t)zrow[j] + lnew);
                     }
                     min1[m] = nm1; min2[m] = nm2; amin[m] = (int8_t)nam;
-                    sbits[m] = (uint32_t)nsb; sprod[m] = (uint8_t)nsp;
+                    sbits[m] = nsb; sprod[m] = (uint8_t)nsp;
                 }
             }
             it = k + 1;

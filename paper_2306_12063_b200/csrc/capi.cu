@@ -1,0 +1,436 @@
+// capi.cu -- the extern "C" boundary of libqcb200.so (declared in include/qcb200.h).
+//
+// Validation mirrors the reference's decoder._check_block / decode_block
+// (/root/reference/pkg/src/qcldpc/decoder.py:179-186, 217-258): errors are
+// reported before any work is queued, the kernels themselves never fail on
+// data.  Outputs are caller-owned, exactly like the reference kernel boundary
+// (_kernels.py:17-19: hard/iters/conv are written in place).
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qcb200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace qcb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail((int)e, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+struct DeviceTables {
+  int32_t* d = nullptr;  // tier_start (mb+1) | ent_j (ne) | ent_e (ne)
+};
+
+}  // namespace
+
+struct qc_code_s {
+  int32_t mb = 0, nb = 0, kb = 0, z = 0, n = 0, ne = 0, max_deg = 0;
+  int32_t structure = -1;            // index into kStructureMasks, -1 = generic only
+  std::vector<int32_t> shifts;       // mb x nb
+  std::vector<int32_t> tier_start, ent_j, ent_e;
+  int32_t enc_y = -1, enc_hb = -1;   // encoder plan (find_y, encoder.py:39-46), -1 if malformed
+  std::mutex mu;
+  std::map<int, DeviceTables> dev;   // generic decoder tables per device
+
+  const int32_t* tables(int device, cudaError_t* err) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(device);
+    if (it != dev.end()) return it->second.d;
+    std::vector<int32_t> host(tier_start);
+    host.insert(host.end(), ent_j.begin(), ent_j.end());
+    host.insert(host.end(), ent_e.begin(), ent_e.end());
+    int32_t* d = nullptr;
+    *err = cudaMalloc(&d, host.size() * sizeof(int32_t));
+    if (*err != cudaSuccess) return nullptr;
+    *err = cudaMemcpy(d, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (*err != cudaSuccess) { cudaFree(d); return nullptr; }
+    dev[device].d = d;
+    return d;
+  }
+};
+
+namespace {
+
+int build_code(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code_t* out) {
+  if (!out) return fail(QC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!shifts || mb < 1 || nb <= mb || z < 1) return fail(QC_EINVAL, "bad code shape mb=%d nb=%d z=%d", mb, nb, z);
+  if ((int64_t)nb * z > (1 << 30)) return fail(QC_EINVAL, "code too long");
+  std::unique_ptr<qc_code_s> c(new (std::nothrow) qc_code_s());
+  if (!c) return fail(QC_ENOMEM, "out of host memory");
+  c->mb = mb; c->nb = nb; c->kb = nb - mb; c->z = z; c->n = nb * z;
+  c->shifts.assign(shifts, shifts + (size_t)mb * nb);
+  c->tier_start.push_back(0);
+  for (int i = 0; i < mb; ++i) {
+    int deg = 0;
+    for (int j = 0; j < nb; ++j) {
+      const int e = shifts[i * nb + j];
+      if (e < -1 || e >= z) return fail(QC_EINVAL, "shift %d at (%d,%d) outside [-1, %d)", e, i, j, z);
+      if (e >= 0) { c->ent_j.push_back(j); c->ent_e.push_back(e); ++deg; }
+    }
+    if (deg > kMaxDeg) return fail(QC_EUNSUPPORTED, "row degree %d > 32 (sign bitmap width)", deg);
+    c->max_deg = std::max(c->max_deg, deg);
+    c->tier_start.push_back((int32_t)c->ent_j.size());
+  }
+  c->ne = (int32_t)c->ent_j.size();
+  // specialised structure?
+  for (int s = 0; s < kNumStructures; ++s) {
+    const StructureMask& m = kStructureMasks[s];
+    if (m.mb != mb || m.nb != nb) continue;
+    bool same = true;
+    for (int i = 0; i < mb && same; ++i) {
+      unsigned row = 0;
+      for (int j = 0; j < nb; ++j) row |= (shifts[i * nb + j] >= 0 ? 1u : 0u) << j;
+      same = row == m.rows[i];
+    }
+    if (same && z * 1 <= 384) { c->structure = s; break; }
+  }
+  // encoder plan: the single interior non-negative entry of the h_b column
+  if (mb >= 3) {
+    int y = -1, cnt = 0;
+    for (int i = 1; i < mb - 1; ++i)
+      if (shifts[i * nb + c->kb] >= 0) { y = i; ++cnt; }
+    if (cnt == 1) { c->enc_y = y; c->enc_hb = shifts[y * nb + c->kb]; }
+  }
+  *out = c.release();
+  return QC_OK;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <typename T>
+int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32_t early_term,
+                  uint8_t* hard, int32_t hard_packed, int32_t* iters, uint8_t* conv, T* post,
+                  cudaStream_t stream) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (w < 0 || max_iters < 0) return fail(QC_EINVAL, "w=%lld max_iters=%d", (long long)w, max_iters);
+  if (w == 0) return QC_OK;
+  if (!llr || !hard || !iters || !conv) return fail(QC_EINVAL, "NULL buffer");
+  if (w > (int64_t)1 << 40) return fail(QC_EINVAL, "batch too large");
+  const int elem = (int)sizeof(T);
+  cudaError_t e;
+  if (c->structure >= 0) {
+    SpecArgs a;
+    memset(&a, 0, sizeof a);
+    a.llr = llr; a.hard = hard; a.iters = iters; a.conv = conv; a.post = post;
+    a.w = w; a.n = c->n; a.z = c->z; a.max_iters = max_iters; a.early_term = early_term ? 1 : 0;
+    a.hard_packed = hard_packed ? 1 : 0;
+    const int rs = spec_row_stride_bytes(elem);
+    const int es = elem * 2;
+    a.pairs = spec_pairs_per_cta(c->z);
+    a.zrs = c->z * rs;
+    a.ps = c->z * rs;
+    for (int i = 0; i < c->ne; ++i) {
+      a.off[i] = c->ent_e[i] * rs + c->ent_j[i] * es;
+      a.thr[i] = c->z - c->ent_e[i];
+    }
+    e = launch_spec(c->structure, elem, a, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "decode (specialised kernel)");
+    return QC_OK;
+  }
+  int device = 0;
+  e = cudaGetDevice(&device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  const int32_t* tab = c->tables(device, &e);
+  if (!tab) return cuda_fail(e, "uploading code tables");
+  GenericArgs a;
+  memset(&a, 0, sizeof a);
+  a.llr = llr; a.hard = hard; a.iters = iters; a.conv = conv; a.post = post;
+  a.w = w; a.n = c->n; a.z = c->z; a.mb = c->mb; a.max_iters = max_iters;
+  a.early_term = early_term ? 1 : 0; a.hard_packed = hard_packed ? 1 : 0;
+  a.tier_start = tab; a.ent_j = tab + c->mb + 1; a.ent_e = tab + c->mb + 1 + c->ne;
+  int g = std::max(1, std::min(64, 256 / std::max(1, c->z)));
+  const size_t limit = 160 * 1024;
+  while (g > 1 && generic_smem_bytes(g, c->n, c->mb * c->z, elem) > limit) --g;
+  if (generic_smem_bytes(g, c->n, c->mb * c->z, elem) > 227 * 1024)
+    return fail(QC_EUNSUPPORTED, "one codeword (N=%d) does not fit in shared memory", c->n);
+  a.cw_per_cta = g;
+  e = launch_generic(a, elem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "decode (generic kernel)");
+  return QC_OK;
+}
+
+// ---- host-buffer path: cached codes and device workspace --------------------
+
+struct HostCtx {
+  std::mutex mu;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  std::map<std::vector<int32_t>, qc_code_t> codes;
+};
+
+HostCtx& host_ctx(int device) {
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<HostCtx>> ctxs;
+  std::lock_guard<std::mutex> lk(m);
+  auto& p = ctxs[device];
+  if (!p) p.reset(new HostCtx());
+  return *p;
+}
+
+int csr_to_shifts(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx, int64_t n_edges,
+                  int32_t mb, int32_t z, int32_t n, std::vector<int32_t>& tab) {
+  if (!row_ptr || !col_idx || mb < 1 || z < 1 || n < 1 || n % z)
+    return fail(QC_EINVAL, "bad CSR shape (mb=%d z=%d n=%d)", mb, z, n);
+  if (row_ptr_len != (int64_t)mb * z + 1) return fail(QC_EINVAL, "row_ptr length %lld != mb*z+1", (long long)row_ptr_len);
+  const int nb = n / z;
+  tab.assign((size_t)mb * nb, -1);
+  for (int i = 0; i < mb; ++i) {
+    const int64_t lo = row_ptr[(int64_t)i * z], hi = row_ptr[(int64_t)i * z + 1];
+    if (lo < 0 || hi < lo || hi > n_edges) return fail(QC_EINVAL, "row_ptr out of range");
+    int prev = -1;
+    for (int64_t p = lo; p < hi; ++p) {
+      const int col = col_idx[p];
+      if (col < 0 || col >= n) return fail(QC_EINVAL, "column %d out of range", col);
+      const int j = col / z;
+      if (j <= prev) return fail(QC_EUNSUPPORTED, "tier %d: block columns not ascending", i);
+      prev = j;
+      tab[(size_t)i * nb + j] = col % z;
+    }
+    // every row of the tier must be the cyclic shift of row i*z
+    for (int r = 0; r < z; ++r) {
+      const int64_t a0 = row_ptr[(int64_t)i * z + r], a1 = row_ptr[(int64_t)i * z + r + 1];
+      if (a1 - a0 != hi - lo) return fail(QC_EUNSUPPORTED, "tier %d: rows differ in degree (not QC)", i);
+      int64_t p = a0;
+      for (int j = 0; j < nb; ++j) {
+        const int e = tab[(size_t)i * nb + j];
+        if (e < 0) continue;
+        if (p >= n_edges || col_idx[p] != j * z + (r + e) % z)
+          return fail(QC_EUNSUPPORTED, "tier %d row %d: CSR is not a quasi-cyclic expansion", i, r);
+        ++p;
+      }
+    }
+  }
+  return QC_OK;
+}
+
+template <typename T>
+int decode_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx, int64_t n_edges,
+                int32_t mb, int32_t z, const T* llrs, int64_t w, int64_t n, int32_t max_iters,
+                int32_t early_term, uint8_t* hard, int32_t* iters, uint8_t* conv) {
+  if (w < 0 || n < 1 || n > (1 << 30)) return fail(QC_EINVAL, "bad w/n");
+  std::vector<int32_t> tab;
+  int rc = csr_to_shifts(row_ptr, row_ptr_len, col_idx, n_edges, mb, z, (int32_t)n, tab);
+  if (rc) return rc;
+  if (w == 0) return QC_OK;
+  if (!llrs || !hard || !iters || !conv) return fail(QC_EINVAL, "NULL buffer");
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  HostCtx& ctx = host_ctx(device);
+  std::lock_guard<std::mutex> lk(ctx.mu);
+  std::vector<int32_t> key(tab);
+  key.push_back(mb); key.push_back(z); key.push_back((int32_t)n);
+  qc_code_t code;
+  auto it = ctx.codes.find(key);
+  if (it == ctx.codes.end()) {
+    rc = build_code(mb, (int32_t)(n / z), z, tab.data(), &code);
+    if (rc) return rc;
+    ctx.codes[key] = code;
+  } else {
+    code = it->second;
+  }
+  for (int i = 0; i < 2; ++i)
+    if (!ctx.st[i]) {
+      e = cudaStreamCreateWithFlags(&ctx.st[i], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    }
+  // chunked, double-buffered: H2D(i+1) overlaps decode(i) (two streams)
+  const int64_t chunk = std::min<int64_t>(w, std::max<int64_t>(2048, ((int64_t)64 << 20) / (n * (int64_t)sizeof(T))));
+  const size_t llr_b = (size_t)chunk * n * sizeof(T), hard_b = (size_t)chunk * n;
+  const size_t need = llr_b + hard_b + (size_t)chunk * 8 + 256;
+  for (int i = 0; i < 2; ++i)
+    if (ctx.cap[i] < need) {
+      if (ctx.buf[i]) cudaFree(ctx.buf[i]);
+      ctx.buf[i] = nullptr; ctx.cap[i] = 0;
+      e = cudaMalloc(&ctx.buf[i], need);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc workspace");
+      ctx.cap[i] = need;
+    }
+  for (int64_t c0 = 0, ci = 0; c0 < w; c0 += chunk, ++ci) {
+    const int b = (int)(ci & 1);
+    const int64_t cw = std::min(chunk, w - c0);
+    char* base = static_cast<char*>(ctx.buf[b]);
+    T* d_llr = reinterpret_cast<T*>(base);
+    uint8_t* d_hard = reinterpret_cast<uint8_t*>(base + llr_b);
+    int32_t* d_it = reinterpret_cast<int32_t*>(base + llr_b + hard_b + 128 - ((llr_b + hard_b) & 127));
+    uint8_t* d_conv = reinterpret_cast<uint8_t*>(d_it + chunk);
+    cudaStream_t s = ctx.st[b];
+    e = cudaMemcpyAsync(d_llr, llrs + c0 * n, (size_t)cw * n * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D llr");
+    rc = decode_device<T>(code, d_llr, cw, max_iters, early_term, d_hard, 0, d_it, d_conv, nullptr, s);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(hard + c0 * n, d_hard, (size_t)cw * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(iters + c0, d_it, (size_t)cw * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(conv + c0, d_conv, (size_t)cw, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H outputs");
+  }
+  for (int i = 0; i < 2; ++i) {
+    e = cudaStreamSynchronize(ctx.st[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "decode (host path)");
+  }
+  return QC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qc_version(void) { return 100; }
+const char* qc_last_error(void) { return g_err.c_str(); }
+
+int qc_code_create(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code_t* out) {
+  return build_code(mb, nb, z, shifts, out);
+}
+
+int qc_code_from_csr(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,
+                     int64_t n_edges, int32_t mb, int32_t z, int32_t n, qc_code_t* out) {
+  std::vector<int32_t> tab;
+  int rc = csr_to_shifts(row_ptr, row_ptr_len, col_idx, n_edges, mb, z, n, tab);
+  if (rc) return rc;
+  return build_code(mb, n / z, z, tab.data(), out);
+}
+
+int qc_code_destroy(qc_code_t code) {
+  if (!code) return QC_OK;
+  for (auto& kv : code->dev) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(kv.first);
+    cudaFree(kv.second.d);
+    cudaSetDevice(cur);
+  }
+  delete code;
+  return QC_OK;
+}
+
+int qc_code_info(qc_code_t c, int32_t* mb, int32_t* nb, int32_t* z, int32_t* n_edges,
+                 int32_t* max_row_degree, int32_t* kernel) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (mb) *mb = c->mb;
+  if (nb) *nb = c->nb;
+  if (z) *z = c->z;
+  if (n_edges) *n_edges = c->ne * c->z;
+  if (max_row_degree) *max_row_degree = c->max_deg;
+  if (kernel) *kernel = c->structure >= 0 ? 1 : 0;
+  return QC_OK;
+}
+
+int qc_decode_f32(qc_code_t code, const float* llr, int64_t w, int32_t max_iters, int32_t early_term,
+                  uint8_t* hard, int32_t hard_packed, int32_t* iters, uint8_t* conv, float* post_out,
+                  void* stream) {
+  return decode_device<float>(code, llr, w, max_iters, early_term, hard, hard_packed, iters, conv,
+                              post_out, as_stream(stream));
+}
+
+int qc_decode_i16(qc_code_t code, const int16_t* llr, int64_t w, int32_t max_iters, int32_t early_term,
+                  uint8_t* hard, int32_t hard_packed, int32_t* iters, uint8_t* conv, int16_t* post_out,
+                  void* stream) {
+  return decode_device<int16_t>(code, llr, w, max_iters, early_term, hard, hard_packed, iters, conv,
+                                post_out, as_stream(stream));
+}
+
+static int grouped(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
+                   int32_t hard_packed, void* stream, bool f32) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(QC_EINVAL, "bad job list");
+  for (int i = 0; i < n_jobs; ++i) {
+    const qc_decode_job_t& j = jobs[i];
+    const int rc = f32 ? decode_device<float>(j.code, (const float*)j.llr, j.w, max_iters, early_term, j.hard,
+                                              hard_packed, j.iters, j.conv, (float*)j.post_out, as_stream(stream))
+                       : decode_device<int16_t>(j.code, (const int16_t*)j.llr, j.w, max_iters, early_term,
+                                                j.hard, hard_packed, j.iters, j.conv, (int16_t*)j.post_out,
+                                                as_stream(stream));
+    if (rc) return rc;
+  }
+  return QC_OK;
+}
+
+int qc_decode_grouped_f32(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
+                          int32_t hard_packed, void* stream) {
+  return grouped(jobs, n_jobs, max_iters, early_term, hard_packed, stream, true);
+}
+
+int qc_decode_grouped_i16(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
+                          int32_t hard_packed, void* stream) {
+  return grouped(jobs, n_jobs, max_iters, early_term, hard_packed, stream, false);
+}
+
+int qc_decode_batch_f32_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,
+                             int64_t n_edges, int32_t mb, int32_t z, const float* llrs, int64_t w, int64_t n,
+                             int32_t max_iters, int32_t early_term, uint8_t* hard, int32_t* iters,
+                             uint8_t* conv) {
+  return decode_host<float>(row_ptr, row_ptr_len, col_idx, n_edges, mb, z, llrs, w, n, max_iters,
+                            early_term, hard, iters, conv);
+}
+
+int qc_decode_batch_i16_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,
+                             int64_t n_edges, int32_t mb, int32_t z, const int16_t* llrs, int64_t w, int64_t n,
+                             int32_t max_iters, int32_t early_term, uint8_t* hard, int32_t* iters,
+                             uint8_t* conv) {
+  return decode_host<int16_t>(row_ptr, row_ptr_len, col_idx, n_edges, mb, z, llrs, w, n, max_iters,
+                              early_term, hard, iters, conv);
+}
+
+int qc_encode_packed(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw, void* stream) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (c->z % 8) return fail(QC_EUNALIGNED, "packed encoder needs z %% 8 == 0, got z=%d", c->z);
+  if (c->enc_y < 0) return fail(QC_EMALFORMED, "h_b column lacks a single interior entry");
+  if (c->mb > 12 || c->nb > 24 || c->z > 128) return fail(QC_EUNSUPPORTED, "encoder supports mb<=12, nb<=24, z<=128");
+  if (w < 0) return fail(QC_EINVAL, "w < 0");
+  if (w == 0) return QC_OK;
+  if (!info || !cw) return fail(QC_EINVAL, "NULL buffer");
+  EncodeArgs a;
+  memset(&a, 0, sizeof a);
+  a.info = info; a.cw = cw; a.w = w; a.mb = c->mb; a.nb = c->nb; a.z = c->z; a.hb_shift = c->enc_hb;
+  for (int i = 0; i < c->mb * c->nb; ++i) a.shifts[i] = c->shifts[i];
+  cudaError_t e = launch_encode_packed(a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "encode_packed");
+  return QC_OK;
+}
+
+int qc_encode_packed_host(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (w < 0) return fail(QC_EINVAL, "w < 0");
+  if (w == 0) return QC_OK;
+  if (!info || !cw) return fail(QC_EINVAL, "NULL buffer");
+  const size_t kb = (size_t)(c->kb * c->z / 8), nbt = (size_t)(c->n / 8);
+  uint8_t *d_in = nullptr, *d_out = nullptr;
+  cudaError_t e = cudaMalloc(&d_in, (size_t)w * kb);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, (size_t)w * nbt);
+  if (e == cudaSuccess) e = cudaMemcpy(d_in, info, (size_t)w * kb, cudaMemcpyHostToDevice);
+  int rc = QC_OK;
+  if (e == cudaSuccess) {
+    rc = qc_encode_packed(c, d_in, w, d_out, nullptr);
+    if (rc == QC_OK) e = cudaMemcpy(cw, d_out, (size_t)w * nbt, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_in);
+  cudaFree(d_out);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "encode_packed (host path)");
+  return QC_OK;
+}
+
+}  // extern "C"

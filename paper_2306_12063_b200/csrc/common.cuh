@@ -1,0 +1,44 @@
+// common.cuh -- shared device definitions for the qcb200 QC-LDPC kernels (sm_100a).
+//
+// Arithmetic traits reproduce the reference kernels' per-edge operations
+// bit for bit (/root/reference/pkg/src/qcldpc/_kernels.py:61-84 float32,
+// :147-170 int16 with two's-complement wrap after every op).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "structures_gen.cuh"
+
+namespace qcb {
+
+constexpr int kMaxDeg = 32;          // sign bitmap width (reference decoder.py:185-186)
+constexpr int kMaxGenericTiers = 256;
+constexpr int kRowStrideUnits = 25;  // padded nb (24 -> 25): odd stride, conflict-free banks
+
+// ---- exact float32 helpers -------------------------------------------------
+__device__ __forceinline__ float f_inf() { return __int_as_float(0x7f800000); }
+__device__ __forceinline__ float f_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float f_add(float a, float b) { return __fadd_rn(a, b); }
+// NaN-propagating max: max.NaN(nm1, NaN) = NaN so that min(nm2, .) keeps nm2,
+// matching the reference's `elif a < nm2` (false for NaN).
+__device__ __forceinline__ float f_max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// ---- int16 wrap helpers -----------------------------------------------------
+__device__ __forceinline__ int sext16(int x) { return (int)(short)x; }
+
+// Magnitude "key": a = |wrap16(zz)| lies in [0, 32768]; the reference keeps it
+// as int16, so 32768 wraps to -32768 and sorts below everything.
+// key = a ^ 0x8000 maps that signed-int16 order onto unsigned [0, 0xFFFF].
+__device__ __forceinline__ unsigned i16_key_of(int zz_wrapped) {
+  return (unsigned)abs(zz_wrapped) ^ 0x8000u;
+}
+// key -> magnitude value (as a 32-bit int; 32768 stands for int16 -32768,
+// harmless because every use is followed by a wrapped add/sub or a 16-bit store)
+__device__ __forceinline__ int i16_val_of_key(unsigned k) { return (int)(k ^ 0x8000u); }
+constexpr unsigned kI16KeyInit = 32767u ^ 0x8000u;  // nm1 = nm2 = 32767 (ref _kernels.py:142-143)
+
+}  // namespace qcb

@@ -1,0 +1,60 @@
+// kernels.h -- internal launch interface between the C-ABI layer (capi.cu)
+// and the device kernels.  Not part of the public ABI (that is include/qcb200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "structures_gen.cuh"
+
+namespace qcb {
+
+struct GenericArgs {
+  const void* llr;
+  void* hard;
+  int32_t* iters;
+  uint8_t* conv;
+  void* post;
+  int64_t w;
+  int32_t n, z, mb, max_iters, early_term, hard_packed, cw_per_cta;
+  const int32_t* tier_start;  // device, mb+1
+  const int32_t* ent_j;       // device, block column per nonzero entry (tier-major, ascending j)
+  const int32_t* ent_e;       // device, shift per nonzero entry
+};
+
+size_t generic_smem_bytes(int cw_per_cta, int n, int m, int elem);
+cudaError_t launch_generic(const GenericArgs& a, int elem, cudaStream_t s);
+
+// Specialised kernels: structure (block columns per tier) is a template
+// parameter, shifts are kernel parameters.  Two codewords per thread.
+struct SpecArgs {
+  const void* llr;
+  void* hard;
+  int32_t* iters;
+  uint8_t* conv;
+  void* post;
+  int64_t w;
+  int32_t n, z, max_iters, early_term, hard_packed;
+  int32_t pairs;   // codeword pairs per CTA
+  int32_t zrs;     // Z * row stride (bytes)
+  int32_t ps;      // pair stride (bytes)
+  int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
+  int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
+};
+
+// returns cudaErrorInvalidValue if no specialised kernel exists for (structure, elem)
+cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
+int spec_row_stride_bytes(int elem);   // RS for the SMEM layout
+int spec_pairs_per_cta(int z);
+
+// Packed direct encoder (encoder.py:166-199), byte-aligned Z.
+struct EncodeArgs {
+  const uint8_t* info;   // W x K/8
+  uint8_t* cw;           // W x N/8
+  int64_t w;
+  int32_t mb, nb, z, hb_shift;
+  int32_t shifts[12 * 24];  // mb x nb, -1 = zero block
+};
+cudaError_t launch_encode_packed(const EncodeArgs& a, cudaStream_t s);
+
+}  // namespace qcb

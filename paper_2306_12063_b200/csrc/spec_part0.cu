@@ -1,0 +1,22 @@
+// spec_part0.cu -- instantiations of the specialised decoder for the
+// structures with ID % 6 == 0 (see decode_spec.cu).
+#include "decode_spec.cuh"
+
+namespace qcb {
+
+cudaError_t launch_spec_part0(int structure_id, int elem, const SpecArgs& a, cudaStream_t s) {
+#define QCB_DISPATCH(STRUCT)                                                                \
+  if constexpr (STRUCT::ID % 6 == 0) {                                                   \
+    if (structure_id == STRUCT::ID) {                                                      \
+      if (elem == 4) return a.early_term ? launch_one<STRUCT, F32Pair, true>(a, s)          \
+                                         : launch_one<STRUCT, F32Pair, false>(a, s);        \
+      return a.early_term ? launch_one<STRUCT, I16Pair, true>(a, s)                         \
+                          : launch_one<STRUCT, I16Pair, false>(a, s);                       \
+    }                                                                                      \
+  }
+  QCB_FOR_EACH_STRUCTURE(QCB_DISPATCH)
+#undef QCB_DISPATCH
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace qcb

@@ -1,0 +1,116 @@
+"""BASELINE.json workloads and seeded synthetic channel inputs.
+
+The five configurations of `/root/repo/BASELINE.json`:
+
+  C1  Wi-Fi 648 R1/2,  f32, 10 it, W = 1024,      Eb/N0 2.0 dB
+  C2  WiMAX 2304 R1/2, f32, 10 it, W = 65536,     Eb/N0 1.5 dB   (bench default)
+  C3  Wi-Fi 1944 R5/6, i16,  8 it, W = 262144,    Eb/N0 4.0 dB
+  C4  18 codes mixed,  f32, 10 it, W = 18 x 16384, Eb/N0 3.0 dB
+  C5  WiMAX 2304 R3/4A, i16, 10 it, W = 2^22,     Eb/N0 2.0 dB (+ packed encode)
+
+Inputs follow the reference channel (chansim.py:26-62, test_acceptance.py:45-54):
+seeded uniform info bits, systematic encoding, BPSK (0 -> +1), AWGN with
+sigma^2 = 1 / (2 R 10^(EbN0/10)), LLR = 2y/sigma^2 in float64, then float32 or
+quantize_llr(q_b=10).  No public dataset is involved.
+
+To build BASELINE-sized batches quickly, `device_llrs` encodes a seeded pool of
+codewords on the host (numpy, exact reference encoder) and tiles it over the
+batch while drawing fresh Gaussian noise for every codeword on the GPU
+(torch Philox, seeded), so every LLR in the batch is distinct.  Decoding
+runs a fixed number of iterations, so the work does not depend on the data.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import codebook as CB
+from .decoder import Arithmetic, DecoderConfig
+from .encoder import encode_array, make_plan
+
+
+@dataclass(frozen=True)
+class Workload:
+    key: str
+    codes: tuple            # ((standard, n_bits, rate), ...)
+    fixed: bool
+    iters: int
+    w_per_code: int
+    ebn0_db: float
+    seed: int
+
+    @property
+    def arithmetic(self) -> Arithmetic:
+        return Arithmetic.Fixed16 if self.fixed else Arithmetic.Float32
+
+    def config(self) -> DecoderConfig:
+        return DecoderConfig(max_iterations=self.iters, arithmetic=self.arithmetic,
+                             early_termination=False)
+
+    def model_matrices(self):
+        return [CB.get_model_matrix(*c) for c in self.codes]
+
+    @property
+    def w_total(self) -> int:
+        return self.w_per_code * len(self.codes)
+
+
+ALL_18 = tuple([("wifi", n, r) for n in (648, 1296, 1944) for r in ("1/2", "2/3", "3/4", "5/6")]
+               + [("wimax", 2304, r) for r in ("1/2", "2/3A", "2/3B", "3/4A", "3/4B", "5/6")])
+
+WORKLOADS = {
+    "C1": Workload("C1", (("wifi", 648, "1/2"),), False, 10, 1024, 2.0, 1),
+    "C2": Workload("C2", (("wimax", 2304, "1/2"),), False, 10, 65536, 1.5, 2),
+    "C3": Workload("C3", (("wifi", 1944, "5/6"),), True, 8, 262144, 4.0, 3),
+    "C4": Workload("C4", ALL_18, False, 10, 16384, 3.0, 4),
+    "C5": Workload("C5", (("wimax", 2304, "3/4A"),), True, 10, 1 << 22, 2.0, 5),
+}
+
+
+def sigma2(ebn0_db: float, rate: float) -> float:
+    """chansim.ebn0_to_sigma2 (/root/reference/pkg/src/qcldpc/chansim.py:26-30)."""
+    return 1.0 / (2.0 * rate * 10.0 ** (ebn0_db / 10.0))
+
+
+def host_llrs(mm, w: int, ebn0_db: float, seed, fixed: bool):
+    """Exact host generation (reference recipe), returns (llr, info bits)."""
+    from .decoder import quantize_llr
+    rng = np.random.default_rng(seed)
+    info = rng.integers(0, 2, size=(w, mm.k), dtype=np.uint8)
+    cw = encode_array(make_plan(mm), info)
+    s2 = sigma2(ebn0_db, mm.rate.fraction)
+    y = (1.0 - 2.0 * cw) + rng.standard_normal(cw.shape) * math.sqrt(s2)
+    llr = (2.0 / s2) * y
+    return (quantize_llr(llr).values if fixed else llr.astype(np.float32)), info
+
+
+def device_llrs(mm, w: int, ebn0_db: float, seed: int, fixed: bool, device, pool: int = 4096,
+                chunk: int = 32768):
+    """(W, N) LLR tensor on `device`: tiled host-encoded codeword pool + fresh device noise.
+
+    Returns (llr tensor, codeword pool (P, N) uint8 tensor); codeword i of the
+    batch carries pool row i % P.
+    """
+    import torch
+    rng = np.random.default_rng([seed, 0])
+    p = min(pool, w) if w > 0 else 1
+    info = rng.integers(0, 2, size=(p, mm.k), dtype=np.uint8)
+    cw = torch.from_numpy(encode_array(make_plan(mm), info)).to(device)
+    s2 = sigma2(ebn0_db, mm.rate.fraction)
+    out = torch.empty((w, mm.n), dtype=torch.int16 if fixed else torch.float32, device=device)
+    g = torch.Generator(device=device).manual_seed(int(seed) * 1_000_003 + 17)
+    sym = (1.0 - 2.0 * cw.to(torch.float64))
+    lim = 1023.0
+    for c0 in range(0, w, chunk):
+        c1 = min(w, c0 + chunk)
+        idx = torch.arange(c0, c1, device=device) % p
+        noise = torch.randn((c1 - c0, mm.n), dtype=torch.float64, device=device, generator=g)
+        llr = (2.0 / s2) * (sym[idx] + math.sqrt(s2) * noise)
+        if fixed:
+            out[c0:c1] = torch.clamp(torch.round(llr * (lim / 24.0)), -lim, lim).to(torch.int16)
+        else:
+            out[c0:c1] = llr.to(torch.float32)
+    return out, cw

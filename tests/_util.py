@@ -34,3 +34,28 @@ def load_case(name: str):
 def sigma2(ebn0_db: float, rate: float) -> float:
     """chansim.ebn0_to_sigma2 (/root/reference/pkg/src/qcldpc/chansim.py:26-30)."""
     return 1.0 / (2.0 * rate * 10.0 ** (ebn0_db / 10.0))
+
+
+def noisy_llrs(mm, frames: int, ebn0_db: float, seed: int, fixed: bool = False):
+    """Seeded BPSK/AWGN channel LLRs 2y/sigma^2 (reference test_acceptance.py:45-54).
+
+    Returns (llr values, info bits, codeword bits); int16 LLRs go through
+    quantize_llr(q_b=10) exactly like the reference's fixed-point inputs.
+    """
+    from paper_2306_12063_b200 import decoder as D, encoder as E
+    rng = np.random.default_rng(seed)
+    info = rng.integers(0, 2, size=(frames, mm.k), dtype=np.uint8)
+    cw = E.encode_array(E.make_plan(mm), info)
+    s2 = sigma2(ebn0_db, mm.rate.fraction)
+    y = (1.0 - 2.0 * cw) + rng.standard_normal(cw.shape) * math.sqrt(s2)
+    llr = (2.0 / s2) * y
+    vals = D.quantize_llr(llr).values if fixed else llr.astype(np.float32)
+    return vals, info, cw
+
+
+def have_gpu() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False

@@ -1,0 +1,285 @@
+"""GPU parity: libqcb200's sm_100a decoder/encoder vs the reference's outputs.
+
+Every test here runs the CUDA path through the C ABI (device entry points via
+`decode_batch`, host entry points via the drop-in `_kernels` / `decode_block`)
+and compares bit for bit -- hard decisions, iteration counts, convergence
+flags and posterior LLR bit patterns -- with
+  * golden fixtures produced by the reference itself (tests/golden, made by
+    tools/make_golden.py), and
+  * the CPU oracle (oracle/qc_oracle.c, pinned to those fixtures in
+    tests/test_oracle_golden.py) on seeded inputs for all 126 codes.
+Tolerance: none.  int16 is bit-exact by definition; float32 is bit-exact
+too (identical IEEE operations in identical order), which is stricter than
+the 1e-5 relative bound north_star allows.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2306_12063_b200 as P  # noqa: E402
+from paper_2306_12063_b200 import _kernels  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from tests._util import golden_cases, load_case, noisy_llrs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(d):
+    arith = P.Arithmetic.Float32 if str(d["arithmetic"]) == "float32" else P.Arithmetic.Fixed16
+    return P.DecoderConfig(max_iterations=int(d["max_iters"]), arithmetic=arith,
+                           early_termination=bool(d["early_term"]))
+
+
+def _bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint16)
+
+
+def _gpu(mm, llr, cfg, posteriors=True, hard_packed=False):
+    out = P.decode_batch(mm, torch.from_numpy(llr).cuda(), cfg, posteriors=posteriors,
+                         hard_packed=hard_packed)
+    torch.cuda.synchronize()
+    return [None if t is None else t.cpu().numpy() for t in out]
+
+
+@pytest.mark.parametrize("name", golden_cases("decode") + golden_cases("special"))
+def test_device_path_matches_reference_goldens(name):
+    d = load_case(name)
+    hard, iters, conv, post = _gpu(d["mm"], d["llr"], _cfg(d))
+    assert np.array_equal(hard, d["hard"])
+    assert np.array_equal(iters, d["iters"])
+    assert np.array_equal(conv, d["conv"])
+    if "post" in d:
+        k = d["post"].shape[0]
+        assert np.array_equal(_bits(post[:k]), _bits(d["post"]))
+    hp, _, _ = _gpu(d["mm"], d["llr"], _cfg(d), posteriors=False, hard_packed=True)
+    assert np.array_equal(hp, d["hard_packed"])
+
+
+@pytest.mark.parametrize("name", golden_cases("decode") + golden_cases("special"))
+def test_dropin_kernel_boundary_matches_goldens(name):
+    """The reference's own kernel signature (_kernels.py:17-19), host buffers."""
+    d = load_case(name)
+    h, llr = d["h"], d["llr"]
+    w = llr.shape[0]
+    hard = np.empty((w, h.n), np.uint8)
+    iters = np.empty(w, np.int32)
+    conv = np.empty(w, np.uint8)
+    fn = _kernels.decode_batch_f32 if llr.dtype == np.float32 else _kernels.decode_batch_i16
+    fn(h.row_ptr, h.row_cols, h.m // h.z, h.z, llr, int(d["max_iters"]), int(d["early_term"]),
+       hard, iters, conv)
+    assert np.array_equal(hard, d["hard"]) and np.array_equal(iters, d["iters"])
+    assert np.array_equal(conv, d["conv"])
+
+
+def test_decode_block_api_matches_goldens():
+    d = load_case("decode_wimax576_r12_f32_et.npz")
+    cfg = _cfg(d)
+    res = P.decode_block(d["h"], P.LlrBlock(d["llr"]), cfg, workers=4, pool="mtx")
+    for w, r in enumerate(res):
+        assert np.array_equal(r.hard_bits, d["hard"][w])
+        assert r.iterations == d["iters"][w] and r.converged == bool(d["conv"][w])
+        assert np.array_equal(r.info_bits, d["hard"][w][:d["mm"].k])
+    one = P.decode(d["h"], P.LlrBlock(d["llr"][3]), cfg)
+    assert np.array_equal(one.hard_bits, d["hard"][3]) and one.iterations == d["iters"][3]
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+@pytest.mark.parametrize("early", [False, True])
+def test_all_126_codes_match_oracle(fixed, early):
+    """Every supported code (12 Wi-Fi + 114 WiMAX), seeded noisy inputs, vs the C oracle."""
+    rng_seed = 100 + 2 * fixed + early
+    for idx, (std, n, rate) in enumerate(P.supported_codes()):
+        mm = P.get_model_matrix(std, n, rate)
+        h = P.expand(mm)
+        ebn0 = 1.5 + 2.0 * mm.rate.fraction
+        llr, _, _ = noisy_llrs(mm, 5, ebn0, seed=rng_seed * 1000 + idx, fixed=fixed)
+        iters = 6 if early else 4
+        cfg = P.DecoderConfig(max_iterations=iters,
+                              arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32,
+                              early_termination=early)
+        hard, it, conv, post = _gpu(mm, llr, cfg)
+        oh, oi, oc, op = O.decode_batch(h, llr, iters, early, workers=4, want_post=True)
+        assert np.array_equal(hard, oh), (std, n, rate)
+        assert np.array_equal(it, oi) and np.array_equal(conv, oc), (std, n, rate)
+        assert np.array_equal(_bits(post), _bits(op)), (std, n, rate)
+
+
+def test_generic_kernel_on_nonstandard_codes():
+    """Codes outside the 18 standard structures take the generic kernel."""
+    rng = np.random.default_rng(7)
+    toy = P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 1, 3, 2, np.array([[0, 0, 0]]))
+    assert not P.code_handle(toy).specialised
+    cases = [(toy, 3)]
+    for z, mb, nb in [(5, 3, 9), (17, 4, 10), (40, 6, 16), (7, 2, 30)]:
+        ent = rng.integers(-1, z, size=(mb, nb))
+        ent[rng.random((mb, nb)) < 0.4] = -1
+        ent[:, 0] = rng.integers(0, z, size=mb)
+        cases.append((P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, z, nb, nb - mb, ent), 5))
+    for mm, iters in cases:
+        h = P.expand(mm)
+        for dt, arith in ((np.float32, P.Arithmetic.Float32), (np.int16, P.Arithmetic.Fixed16)):
+            if dt == np.float32:
+                llr = rng.standard_normal((9, mm.n)).astype(np.float32) * 2
+            else:
+                llr = rng.integers(-600, 600, size=(9, mm.n)).astype(np.int16)
+            for early in (False, True):
+                cfg = P.DecoderConfig(max_iterations=iters, arithmetic=arith, early_termination=early)
+                hard, it, conv, post = _gpu(mm, llr, cfg)
+                oh, oi, oc, op = O.decode_batch(h, llr, iters, early, want_post=True)
+                assert np.array_equal(hard, oh) and np.array_equal(it, oi) and np.array_equal(conv, oc)
+                assert np.array_equal(_bits(post), _bits(op))
+
+
+def test_known_answers(golden_dir):
+    kat = np.load(golden_dir / "kat.npz")
+    toy = P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 1, 3, 2, np.array([[0, 0, 0]]))
+    cfg1 = P.DecoderConfig(max_iterations=1, early_termination=False)
+    _, _, _, post = _gpu(toy, np.array([[3.0, -1.0, 2.0]], np.float32), cfg1)
+    assert np.array_equal(post[0], [2.0, 1.0, 1.0])
+    cfg16 = P.DecoderConfig(max_iterations=1, arithmetic=P.Arithmetic.Fixed16, early_termination=False)
+    _, _, _, post = _gpu(toy, np.array([[-32768, 5, 7]], np.int16), cfg16)
+    assert np.array_equal(post[0], kat["wrap_post"])
+    r = P.decode(P.expand(toy), P.LlrBlock(np.zeros(3, np.float32)), P.DecoderConfig(max_iterations=3))
+    assert np.array_equal(r.hard_bits, [1, 1, 1]) and r.iterations == 3 and not r.converged
+
+
+def test_noiseless_converges_in_one_iteration():
+    mm = P.get_model_matrix("wifi", 648, "1/2")
+    rng = np.random.default_rng(3)
+    info = rng.integers(0, 2, (4, mm.k), dtype=np.uint8)
+    cw = P.encode_array(P.make_plan(mm), info)
+    llr = ((1.0 - 2.0 * cw) * 8.0).astype(np.float32)
+    hard, it, conv = _gpu(mm, llr, P.DecoderConfig(), posteriors=False)
+    assert conv.all() and (it == 1).all() and np.array_equal(hard, cw)
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+def test_sign_gauge_symmetry(fixed):
+    """Flipping LLR signs on a codeword's support XORs the decision with it
+    (reference test_decoder.py:149-163)."""
+    mm = P.get_model_matrix("wimax", 2304, "1/2")
+    llr, _, _ = noisy_llrs(mm, 64, 1.5, seed=4, fixed=fixed)
+    cw = P.encode_array(P.make_plan(mm), np.random.default_rng(5).integers(0, 2, mm.k, dtype=np.uint8))
+    flip = (llr * (1 - 2 * cw.astype(np.int32))).astype(llr.dtype)
+    cfg = P.DecoderConfig(arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
+    a = _gpu(mm, llr, cfg, posteriors=False)
+    b = _gpu(mm, flip, cfg, posteriors=False)
+    assert np.array_equal(a[0] ^ cw, b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_batch_partition_invariance():
+    """Outputs do not depend on how the batch is cut (the worker-invariance
+    contract, reference test_decoder.py:228-242): whole batch == slices ==
+    a permutation of the batch."""
+    mm = P.get_model_matrix("wifi", 1944, "5/6")
+    llr, _, _ = noisy_llrs(mm, 301, 4.0, seed=11, fixed=True)
+    cfg = P.DecoderConfig(max_iterations=8, arithmetic=P.Arithmetic.Fixed16, early_termination=True)
+    full = _gpu(mm, llr, cfg)
+    for cut in (1, 7, 150):
+        parts = [_gpu(mm, llr[i:i + cut], cfg) for i in range(0, 301, cut)]
+        for k in range(4):
+            assert np.array_equal(np.concatenate([p[k] for p in parts]), full[k])
+    perm = np.random.default_rng(1).permutation(301)
+    sh = _gpu(mm, llr[perm], cfg)
+    for k in range(4):
+        assert np.array_equal(sh[k], full[k][perm])
+
+
+def test_empty_and_tiny_batches():
+    mm = P.get_model_matrix("wimax", 576, "1/2")
+    h = P.expand(mm)
+    cfg = P.DecoderConfig()
+    assert P.decode_block(h, P.LlrBlock(np.empty((0, h.n), np.float32)), cfg) == []
+    one = P.decode_block(h, P.LlrBlock(np.zeros((1, h.n), np.float32) + 5.0), cfg)
+    assert len(one) == 1 and one[0].converged and one[0].iterations == 1
+    out = P.decode_batch(mm, torch.zeros((0, h.n), device="cuda"), cfg)
+    assert out[0].shape == (0, h.n)
+
+
+@pytest.mark.parametrize("config", ["C2", "C3"])
+def test_full_size_batch_properties(config):
+    """BASELINE sizes: full batch on the GPU, a seeded sample checked against the
+    oracle, and size-independent properties on all of it (packed == packbits of
+    unpacked, conv <=> zero syndrome, posterior signs == hard bits)."""
+    if config == "C2":
+        mm, w, fixed, ebn0, iters = P.get_model_matrix("wimax", 2304, "1/2"), 65536, False, 1.5, 10
+    else:
+        mm, w, fixed, ebn0, iters = P.get_model_matrix("wifi", 1944, "5/6"), 262144, True, 4.0, 8
+    h = P.expand(mm)
+    base, _, _ = noisy_llrs(mm, 4096, ebn0, seed=2, fixed=fixed)
+    llr = np.concatenate([base] * (w // 4096))
+    cfg = P.DecoderConfig(max_iterations=iters, early_termination=False,
+                          arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
+    t = torch.from_numpy(llr).cuda()
+    hard, it, conv, post = P.decode_batch(mm, t, cfg, posteriors=True)
+    hp, _, _ = P.decode_batch(mm, t, cfg, hard_packed=True)
+    torch.cuda.synchronize()
+    hard, it, conv, post, hp = (x.cpu().numpy() for x in (hard, it, conv, post, hp))
+    assert np.array_equal(np.packbits(hard, axis=-1), hp)
+    assert (it == iters).all()
+    assert np.array_equal(hard, (post <= 0).astype(np.uint8))
+    # repeated blocks decode identically wherever they sit in the batch
+    blocks = hard.reshape(-1, 4096, h.n)
+    assert all(np.array_equal(blocks[0], b) for b in blocks[1:])
+    sample = np.random.default_rng(0).choice(4096, 512, replace=False)
+    oh, oi, oc, op = O.decode_batch(h, base[sample], iters, False, want_post=True)
+    assert np.array_equal(hard[sample], oh) and np.array_equal(conv[sample], oc)
+    assert np.array_equal(_bits(post[sample]), _bits(op))
+    par = P.row_parities(h, hard[:2048])
+    assert np.array_equal(conv[:2048] == 1, ~par.any(axis=-1))
+
+
+# --- encoder ------------------------------------------------------------------
+
+def test_packed_encoder_matches_reference_goldens(golden_dir):
+    z = np.load(golden_dir / "encode_packed.npz")
+    n_checked = 0
+    for key in z.files:
+        if not key.startswith("cw_"):
+            continue
+        _, n, rate, wb = key.split("_")
+        mm = P.get_model_matrix("wimax", int(n), rate[0] + "/" + rate[1:])
+        plan = P.make_plan(mm, P.EncoderVariant.Packed, word_bits=int(wb))
+        info = z[f"info_{n}_{rate}"]
+        assert np.array_equal(P.encode_packed(plan, info), z[key]), key
+        dev = P.encode_packed(plan, torch.from_numpy(info).cuda()).cpu().numpy()
+        assert np.array_equal(dev, z[key]), key
+        n_checked += 1
+    assert n_checked >= 20
+
+
+def test_packed_encoder_all_octet_codes_vs_oracle_and_array():
+    rng = np.random.default_rng(1003)
+    codes = [(n, r) for s, n, r in P.supported_codes() if s is P.Standard.Wimax and (n // 24) % 8 == 0]
+    assert len(codes) == 60
+    for n, rate in codes:
+        mm = P.get_model_matrix("wimax", n, rate)
+        info = rng.integers(0, 2, size=(300, mm.k), dtype=np.uint8)
+        ib = P.pack_bits(info)
+        got = P.encode_packed(P.make_plan(mm, P.EncoderVariant.Packed), ib)
+        assert np.array_equal(got, O.encode_packed(mm, ib)), (n, rate)
+        assert np.array_equal(got, P.pack_bits(P.encode_array(P.make_plan(mm), info))), (n, rate)
+
+
+def test_encode_then_decode_round_trip_c5_scale():
+    """2^20 seeded info words (BASELINE config 5 code) -> GPU encode -> noiseless
+    LLRs -> GPU decode converges in one iteration and returns the info bits."""
+    mm = P.get_model_matrix("wimax", 2304, "3/4A")
+    plan = P.make_plan(mm, P.EncoderVariant.Packed)
+    w = 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(5)
+    info = torch.randint(0, 256, (w, mm.k // 8), dtype=torch.uint8, device="cuda", generator=g)
+    cw = P.encode_packed(plan, info)
+    assert torch.equal(cw[:, :mm.k // 8], info)
+    sample = torch.randint(0, w, (2048,), device="cuda", generator=g)
+    ref = O.encode_packed(mm, info[sample].cpu().numpy())
+    assert np.array_equal(cw[sample].cpu().numpy(), ref)
+    bits = torch.from_numpy(np.unpackbits(cw[:65536].cpu().numpy(), axis=-1)).cuda()
+    llr = ((1 - 2 * bits.to(torch.int16)) * 300).to(torch.int16)
+    cfg = P.DecoderConfig(arithmetic=P.Arithmetic.Fixed16)
+    hard, it, conv = P.decode_batch(mm, llr, cfg, hard_packed=True)
+    assert bool(conv.all()) and bool((it == 1).all())
+    assert torch.equal(hard, cw[:65536])
