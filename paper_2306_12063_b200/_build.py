@@ -21,13 +21,14 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "build"
-LIB = PKG / "libqcb200.so"
+OBJ = PKG / os.environ.get("QCB_BUILD_DIR", "build")
+LIB = Path(os.environ.get("QCB_LIB") or PKG / "libqcb200.so")
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-I", str(CSRC), "-I", str(INCLUDE)]
+EXTRA = os.environ.get("QCB_NVCC_EXTRA", "").split()   # tuning experiments only
 
 
 def nvcc() -> str:
@@ -54,7 +55,7 @@ def _stale(target: Path, inputs) -> bool:
 
 def _compile(src: Path, verbose: bool) -> Path:
     obj = OBJ / (src.stem + ".o")
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *NVCC_FLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -8,6 +8,7 @@ raises `NativeLibraryError` loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -16,7 +17,7 @@ import numpy as np
 from .errors import (CodecError, DeviceError, MalformedHb, NativeLibraryError,
                      SizeMismatch, UnsupportedCode, UnsupportedZ)
 
-LIB_PATH = Path(__file__).resolve().parent / "libqcb200.so"
+LIB_PATH = Path(os.environ.get("QCB_LIB") or Path(__file__).resolve().parent / "libqcb200.so")
 
 QC_OK = 0
 QC_EINVAL = -1

@@ -28,7 +28,15 @@ __device__ __forceinline__ float f_max_nan(float a, float b) {
 }
 
 // ---- int16 wrap helpers -----------------------------------------------------
-__device__ __forceinline__ int sext16(int x) { return (int)(short)x; }
+// Wrap to int16 and sign-extend.  Done in PTX on purpose: NVVM folds C++
+// narrowing casts of out-of-range values using value-range facts (e.g. it
+// turns `(int16_t)abs(x) < 32767` into `abs(x) != 32767`, losing the
+// abs(-32768) == -32768 wrap the reference relies on).
+__device__ __forceinline__ int sext16(int x) {
+  int r;
+  asm("cvt.s32.s16 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 
 // Magnitude "key": a = |wrap16(zz)| lies in [0, 32768]; the reference keeps it
 // as int16, so 32768 wraps to -32768 and sorts below everything.

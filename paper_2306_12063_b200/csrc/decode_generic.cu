@@ -37,10 +37,11 @@ struct GenericArith<int16_t> {
   __device__ static int16_t init() { return 32767; }
   __device__ static int16_t load(const int16_t* p) { return *p; }
   __device__ static void store(int16_t* p, int16_t v) { *p = v; }
-  __device__ static int16_t neg(int16_t m) { return (int16_t)(-(int)m); }
-  __device__ static int16_t sub(int16_t a, int16_t b) { return (int16_t)((int)a - (int)b); }
-  __device__ static int16_t add(int16_t a, int16_t b) { return (int16_t)((int)a + (int)b); }
-  __device__ static int16_t absv(int16_t x) { return (int16_t)(x < 0 ? -(int)x : (int)x); }
+  // every op wraps through sext16 (PTX cvt), see common.cuh
+  __device__ static int16_t neg(int16_t m) { return (int16_t)sext16(-(int)m); }
+  __device__ static int16_t sub(int16_t a, int16_t b) { return (int16_t)sext16((int)a - (int)b); }
+  __device__ static int16_t add(int16_t a, int16_t b) { return (int16_t)sext16((int)a + (int)b); }
+  __device__ static int16_t absv(int16_t x) { return (int16_t)sext16(x < 0 ? -(int)x : (int)x); }
 };
 
 template <typename T>

@@ -2,6 +2,7 @@
 // The kernel template lives in decode_spec.cuh; its 18 structures x 2
 // arithmetics x 2 (early termination on/off) instantiations are split over
 // spec_part{0..5}.cu so they compile in parallel.
+#include "decode_f32.cuh"
 #include "decode_spec.cuh"
 
 namespace qcb {
@@ -25,9 +26,10 @@ cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStrea
   }
 }
 
-int spec_row_stride_bytes(int elem) { return kRowStrideUnits * (elem == 4 ? F32Pair::ES : I16Pair::ES); }
+int spec_row_stride_bytes(int elem) { return elem == 4 ? kRsF32 : kRowStrideUnits * I16Pair::ES; }
 
-int spec_pairs_per_cta(int z) {
+int spec_group_per_cta(int elem, int z) {
+  if (elem == 4) return f32_cw_per_cta(z);
   // pick pairs so that pairs*Z fills whole warps well, 96..384 threads
   int best = 1;
   double best_eff = 0.0;

@@ -35,7 +35,8 @@ struct SpecArgs {
   void* post;
   int64_t w;
   int32_t n, z, max_iters, early_term, hard_packed;
-  int32_t pairs;   // codeword pairs per CTA
+  int32_t pairs;   // int16: codeword pairs per CTA; float32: codewords per CTA
+  uint32_t k_one, k_sign, k_shr;  // 1, 2^31, 2^31+1: IMAD multipliers kept out of ptxas' reach
   int32_t zrs;     // Z * row stride (bytes)
   int32_t ps;      // pair stride (bytes)
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
@@ -44,8 +45,8 @@ struct SpecArgs {
 
 // returns cudaErrorInvalidValue if no specialised kernel exists for (structure, elem)
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
-int spec_row_stride_bytes(int elem);   // RS for the SMEM layout
-int spec_pairs_per_cta(int z);
+int spec_row_stride_bytes(int elem);   // RS for the SMEM layout (bytes per c-row)
+int spec_group_per_cta(int elem, int z);  // float32: codewords per CTA, int16: pairs per CTA
 
 // Packed direct encoder (encoder.py:166-199), byte-aligned Z.
 struct EncodeArgs {

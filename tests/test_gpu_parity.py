@@ -159,15 +159,20 @@ def test_noiseless_converges_in_one_iteration():
 @pytest.mark.parametrize("fixed", [False, True])
 def test_sign_gauge_symmetry(fixed):
     """Flipping LLR signs on a codeword's support XORs the decision with it
-    (reference test_decoder.py:149-163)."""
-    mm = P.get_model_matrix("wimax", 2304, "1/2")
-    llr, _, _ = noisy_llrs(mm, 64, 1.5, seed=4, fixed=fixed)
+    (reference test_decoder.py:149-163, same code / SNR / frame count: the
+    symmetry is exact only while int16 never wraps, as in the reference)."""
+    mm = P.get_model_matrix("wimax", 576, "1/2")
+    llr, _, _ = noisy_llrs(mm, 6, 2.0, seed=4, fixed=fixed)
     cw = P.encode_array(P.make_plan(mm), np.random.default_rng(5).integers(0, 2, mm.k, dtype=np.uint8))
     flip = (llr * (1 - 2 * cw.astype(np.int32))).astype(llr.dtype)
     cfg = P.DecoderConfig(arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
     a = _gpu(mm, llr, cfg, posteriors=False)
     b = _gpu(mm, flip, cfg, posteriors=False)
     assert np.array_equal(a[0] ^ cw, b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    h = P.expand(mm)
+    for x, got in ((llr, a), (flip, b)):
+        want = O.decode_batch(h, x, 10, True)
+        assert all(np.array_equal(u, v) for u, v in zip(got, want))
 
 
 def test_batch_partition_invariance():

@@ -1,0 +1,6 @@
+for lib in libqcb200.so libqcb200_minb2.so libqcb200_minb3.so; do
+  for cw in 1 2 4; do
+    echo "== $lib cw=$cw"
+    QCB_LIB=$PWD/paper_2306_12063_b200/$lib QCB_F32_CW=$cw python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'], d['ms_per_step'])"
+  done
+done
