@@ -41,7 +41,10 @@
 
 namespace qcb {
 
-constexpr int kF32MaxThreads = 384;
+#ifndef QCB_F32_MAXT
+#define QCB_F32_MAXT 384
+#endif
+constexpr int kF32MaxThreads = QCB_F32_MAXT;
 constexpr int kF32MaxCw = 16;
 
 // integer ops kept on the FMA pipe: the multipliers come from the parameter
@@ -61,34 +64,28 @@ __device__ __forceinline__ void add_if_neg(uint32_t& acc, float z, uint32_t bit,
   asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
       : "+r"(acc) : "f"(z), "r"(bit), "r"(one));
 }
-// e = (|z| == nm1); sel = e ? n2 : n1; am += e ? bit : 0
-__device__ __forceinline__ uint32_t sel_eq(float z, float nm1, uint32_t n1, uint32_t n2, uint32_t& am,
-                                           uint32_t bit, uint32_t one) {
-  uint32_t s;
-  asm("{\n\t.reg .pred p;\n\t.reg .f32 t;\n\tabs.f32 t, %2;\n\tsetp.eq.f32 p, t, %3;\n\t"
-      "selp.b32 %0, %5, %4, p;\n\t@p mad.lo.u32 %1, %6, %7, %1;\n\t}"
-      : "=r"(s), "+r"(am) : "f"(z), "f"(nm1), "r"(n1), "r"(n2), "r"(bit), "r"(one));
-  return s;
+// |z| == nm1 ? n2 : n1   (nm2 exactly when edge k was the/an argmin; on a tie
+// nm2 == nm1, so this equals the reference's (k == argmin) choice)
+__device__ __forceinline__ uint32_t sel_eq(float z, float nm1, uint32_t n1, uint32_t n2) {
+  return fabsf(z) == nm1 ? n2 : n1;
 }
 
-struct RowF32 {
-  uint32_t m1s, m2s, wa, ws;
-};
-
-template <int D, bool PACK>
-__device__ __forceinline__ void row_update_f32(const float (&p)[D], float (&o)[D], RowF32& s,
+// One check row's update with explicit check-to-variable messages.
+// msg[k] holds L_mn of edge k from the previous sweep (L_old); it is
+// replaced by L_new.  The reference keeps the same information compressed
+// (min1, min2, argmin, sign bitmap, parity; _kernels.py:80-84) and
+// reconstructs L_old from it (:62-63); holding the reconstructed values in
+// registers instead removes that reconstruction from the inner loop and is
+// bit-identical: L_old_k of sweep i+1 *is* L_new_k of sweep i.
+template <int D>
+__device__ __forceinline__ void row_update_f32(const float (&p)[D], float (&o)[D], float* msg,
                                                uint32_t one, uint32_t sign, uint32_t shr) {
-  const uint32_t wa = s.wa;
-  uint32_t vs = PACK ? (s.wa >> 16) : s.ws;
   float zz[D];
   uint32_t nsb = 0;
-  // ---- pass 1: L_old, zz = post - L_old, sign bits (_kernels.py:61-75) -----
+  // ---- pass 1: zz = post - L_old, sign bits (_kernels.py:61-75) -------------
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const uint32_t msel = ((wa >> k) & 1u) ? s.m2s : s.m1s;
-    const uint32_t lold = imad(vs, sign, msel);        // + ws_k * 2^31: sign of L_old
-    vs = imulhi(vs, shr);                               // next bit
-    zz[k] = f_sub(p[k], __uint_as_float(lold));
+    zz[k] = f_sub(p[k], msg[k]);
     add_if_neg(nsb, zz[k], 1u << k, one);
   }
   // ---- min1 / min2 over |zz| (two edges per step) ---------------------------
@@ -108,21 +105,14 @@ __device__ __forceinline__ void row_update_f32(const float (&p)[D], float (&o)[D
   // ---- pass 2: L_new and post = zz + L_new (_kernels.py:76-79) -------------
   const uint32_t ps = imad(__popc(nsb), sign, 0u);      // sign-product parity in bit 31
   const uint32_t n1s = __float_as_uint(nm1) + ps, n2s = __float_as_uint(nm2) + ps;
-  uint32_t vn = nsb, am = 0;
+  uint32_t vn = nsb;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    const uint32_t msel = sel_eq(zz[k], nm1, n1s, n2s, am, 1u << k, one);
-    const uint32_t lnew = imad(vn, sign, msel);         // sign = parity ^ (zz_k < 0)
+    const uint32_t msel = sel_eq(zz[k], nm1, n1s, n2s);
+    const float lnew = __uint_as_float(imad(vn, sign, msel));   // sign = parity ^ (zz_k < 0)
     vn = imulhi(vn, shr);
-    o[k] = f_add(zz[k], __uint_as_float(lnew));
-  }
-  s.m1s = n1s;
-  s.m2s = n2s;
-  if (PACK) {
-    s.wa = am | (nsb << 16);
-  } else {
-    s.wa = am;
-    s.ws = nsb;
+    msg[k] = lnew;
+    o[k] = f_add(zz[k], lnew);
   }
 }
 
@@ -149,11 +139,9 @@ __device__ __forceinline__ void tier_addrs(const SpecArgs& a, int r, uint32_t b0
 
 template <class S, int ZS, bool ET>
 struct F32Decoder {
-  static constexpr bool PACK = S::MAXDEG <= 16;
-
   template <int T>
   __device__ __forceinline__ static void tier(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
-                                              RowF32 (&st)[S::MB]) {
+                                              float (&msg)[S::NE]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
@@ -161,7 +149,7 @@ struct F32Decoder {
     tier_addrs<S, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
     for (int k = 0; k < D; ++k) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(p[k]) : "r"(addr[k]));
-    row_update_f32<D, PACK>(p, o, st[T], a.k_one, a.k_sign, a.k_shr);
+    row_update_f32<D>(p, o, msg + E0, a.k_one, a.k_sign, a.k_shr);
 #pragma unroll
     for (int k = 0; k < D; ++k) asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[k]), "f"(o[k]) : "memory");
   }
@@ -184,8 +172,8 @@ struct F32Decoder {
 
   template <int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
-                                               RowF32 (&st)[S::MB], bool work, std::integer_sequence<int, Ts...>) {
-    ((work ? tier<Ts>(a, r, b0, b1, st) : void(), __syncthreads()), ...);
+                                               float (&msg)[S::NE], bool work, std::integer_sequence<int, Ts...>) {
+    ((work ? tier<Ts>(a, r, b0, b1, msg) : void(), __syncthreads()), ...);
   }
 
   template <int... Ts>
@@ -195,11 +183,19 @@ struct F32Decoder {
   }
 };
 
-#ifndef QCB_F32_MINB
-#define QCB_F32_MINB 1
+// Register cap: the messages (S::NE floats) plus ~52 for the widest tier's
+// transients.  Measured on C2 (NE = 76): 161 regs uncapped -> 4 CTAs of 96
+// threads per SM, 45.9 Gb/s; capped at 128 -> 5 CTAs, 50.3 Gb/s; capped at
+// 96 -> spills, 43.0 Gb/s.
+#ifndef QCB_F32_REG_SLACK
+#define QCB_F32_REG_SLACK 52
 #endif
+template <class S>
+constexpr int f32_reg_cap() {
+  return (S::NE + QCB_F32_REG_SLACK + 7) / 8 * 8 > 255 ? 255 : (S::NE + QCB_F32_REG_SLACK + 7) / 8 * 8;
+}
 template <class S, int ZS, bool ET>
-__global__ void __launch_bounds__(kF32MaxThreads, QCB_F32_MINB) decode_f32_kernel(const __grid_constant__ SpecArgs a) {
+__global__ void __launch_bounds__(kF32MaxThreads) __maxnreg__(f32_reg_cap<S>()) decode_f32_kernel(const __grid_constant__ SpecArgs a) {
   using Dec = F32Decoder<S, ZS, ET>;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[kF32MaxCw], s_done[kF32MaxCw], s_iters[kF32MaxCw];
@@ -242,14 +238,16 @@ __global__ void __launch_bounds__(kF32MaxThreads, QCB_F32_MINB) decode_f32_kerne
   }
   __syncthreads();
 
-  RowF32 st[S::MB];
+  // check-to-variable messages of this thread's rows, all tiers (registers);
+  // the reference starts from min1 = min2 = 0 with no signs: L = +0.0
+  float msg[S::NE];
 #pragma unroll
-  for (int t = 0; t < S::MB; ++t) st[t] = RowF32{0u, 0u, 0u, 0u};  // min1 = min2 = 0, no signs
+  for (int e = 0; e < S::NE; ++e) msg[e] = 0.0f;
 
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   for (int k = 0; k < a.max_iters; ++k) {
     const bool work = act && !(ET && s_done[g]);
-    Dec::sweep(a, r, b0, b1, st, work, tiers);
+    Dec::sweep(a, r, b0, b1, msg, work, tiers);
     const bool last = (k + 1 == a.max_iters);
     if (ET || last) {
       if (tid < kF32MaxCw) s_fail[tid] = 0;
