@@ -138,14 +138,11 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
     a.w = w; a.n = c->n; a.z = c->z; a.max_iters = max_iters; a.early_term = early_term ? 1 : 0;
     a.hard_packed = hard_packed ? 1 : 0;
     const int rs = spec_row_stride_bytes(elem);
-    const int es = elem == 4 ? 4 : 4;   // float32: 4-byte cells (1 codeword); int16: 2 x int16 cells
-    a.pairs = spec_group_per_cta(elem, c->z);
-    a.k_one = 1u; a.k_sign = 0x80000000u; a.k_shr = 0x80000001u;
-    a.zrs = c->z * rs;
-    a.ps = c->z * rs;
+    a.pairs = spec_cw_per_cta(c->z, w);
+    a.k_one = 1u; a.k_sign = 0x80000000u; a.k_shr = 0x80000001u; a.k_neg1 = 0xFFFFFFFFu;
     for (int i = 0; i < c->ne; ++i) {
-      a.off[i] = c->ent_e[i] * rs + c->ent_j[i] * es;
-      a.thr[i] = c->z - c->ent_e[i];
+      a.off[i] = c->ent_e[i] * rs + c->ent_j[i] * elem;   // (e * 25 + j) cells
+      a.thr[i] = c->z - c->ent_e[i];                      // row r wraps when r >= Z - e
     }
     e = launch_spec(c->structure, elem, a, stream);
     if (e != cudaSuccess) return cuda_fail(e, "decode (specialised kernel)");

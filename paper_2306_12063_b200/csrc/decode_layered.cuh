@@ -1,0 +1,449 @@
+// decode_layered.cuh -- layered single-scan min-sum on sm_100a for the 18
+// standard base-matrix structures, float32 and wrap-around int16.
+//
+// Reference: /root/reference/pkg/src/qcldpc/_kernels.py:17-100 (float32) and
+// :103-186 (int16).  Bit-exact: every value the reference computes
+// (zz = post - L_old, |zz|, min1/min2, L_new, post = zz + L_new,
+// hard = post <= 0, the syndrome) is produced by the same float32 / int16
+// operation on the same operands; only the way selections are made differs.
+//
+// Mapping (why, with the ncu evidence):
+//  * one thread = one check row r of every tier of ONE codeword; a CTA holds
+//    G codewords (G*Z threads); tiers run in sequence with one CTA barrier
+//    between them (layered schedule); the Z rows of a tier touch disjoint
+//    columns, so running them concurrently equals the reference's row loop;
+//  * posteriors live in shared memory as [cw][c][j] (c = position inside the
+//    circulant, j = block column, rows padded to 25 columns); the cyclic
+//    shift of edge (j, e) is the indexed shared-memory read at
+//    ((r + e) mod Z) * 25 + j -- no expanded H anywhere.  For the 18 native
+//    codes Z and the shifts are compile-time constants (one ISETP + one SEL
+//    per edge, circulant offset folded into the LDS immediate); scaled WiMAX
+//    codes take them from the kernel parameter block;
+//  * the check-to-variable messages of a thread's rows are held explicitly,
+//    one register per edge (the reference keeps them compressed as
+//    min1/min2/argmin/sign bits and rebuilds L_old every sweep,
+//    _kernels.py:62-63; keeping the rebuilt values is bit-identical and
+//    removes that work from the inner loop);
+//  * instruction mix is chosen for the measured pipe rates (tools/pipebench):
+//    FADD is full rate, IMAD / VIADD.16x2 share the half-rate FMA-heavy pipe,
+//    compare / select / logic / min-max share the half-rate ALU pipe and
+//    IMAD.HI is quarter rate, so sign handling rides on IMAD and min/max
+//    are tracked two edges per step with 3-input min.
+#pragma once
+#include <cstdlib>
+#include <utility>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace qcb {
+
+constexpr int kLayMaxThreads = 384;
+constexpr int kLayMaxCw = 16;
+
+// ---------------------------------------------------------------------------
+// small PTX helpers: multipliers come from the parameter block (constant bank)
+// so ptxas keeps them as IMAD (FMA-heavy pipe) instead of ALU shifts
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t imulhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// acc += bit if z < 0 (exact "< 0": -0.0 and NaN do not count, _kernels.py:73)
+__device__ __forceinline__ void add_if_neg_f32(uint32_t& acc, float z, uint32_t bit, uint32_t one) {
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
+      : "+r"(acc) : "f"(z), "r"(bit), "r"(one));
+}
+// acc += bit if bit 15 of d is set (int16 "zz < 0", _kernels.py:159)
+__device__ __forceinline__ void add_if_neg_i16(uint32_t& acc, uint32_t d, uint32_t bit, uint32_t one) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, 0x8000;\n\tsetp.ne.u32 p, t, 0;\n\t"
+      "@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
+      : "+r"(acc) : "r"(d), "r"(bit), "r"(one));
+}
+// 16-bit signed lane ops on the low halves (high halves are don't-care)
+__device__ __forceinline__ uint32_t vmin16(uint32_t a, uint32_t b) {
+  uint32_t d; asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+__device__ __forceinline__ uint32_t vmax16(uint32_t a, uint32_t b) {
+  uint32_t d; asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+
+struct RtK {              // runtime constants (kernel parameters)
+  uint32_t one, sign, shr, neg1;
+};
+
+// ---------------------------------------------------------------------------
+// float32 row update (_kernels.py:49-84), messages msg[k] = L_mn of edge k
+// ---------------------------------------------------------------------------
+struct ArithF32 {
+  using Val = float;                     // posterior / message value
+  static constexpr int kElem = 4;        // bytes per shared-memory cell
+
+  __device__ static Val lds(uint32_t a) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
+  __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+  __device__ static bool hard(Val v) { return v <= 0.0f; }
+  __device__ static Val zero() { return 0.0f; }   // reference init: min1 = min2 = 0, no signs -> L = +0.0
+
+  template <int D>
+  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
+    float zz[D];
+    uint32_t nsb = 0;
+    // pass 1: zz = post - L_old, sign bits (_kernels.py:61-75)
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      zz[k] = f_sub(p[k], msg[k]);
+      add_if_neg_f32(nsb, zz[k], 1u << k, K.one);
+    }
+    // min1 / min2 of |zz|, two edges per step; max.NaN keeps NaN out of min2
+    // exactly like the reference's `elif a < nm2`
+    float nm1 = f_inf(), nm2 = f_inf();
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) {
+      const float x = fabsf(zz[k]), y = fabsf(zz[k + 1]);
+      const float lo = fminf(x, y), hi = f_max_nan(x, y);
+      nm2 = fminf(nm2, fminf(hi, f_max_nan(nm1, lo)));
+      nm1 = fminf(nm1, lo);
+    }
+    if (D & 1) {
+      const float x = fabsf(zz[D - 1]);
+      nm2 = fminf(nm2, f_max_nan(nm1, x));
+      nm1 = fminf(nm1, x);
+    }
+    // pass 2 (_kernels.py:76-79): |L_new| = nm2 iff |zz_k| == nm1 (on a tie
+    // nm2 == nm1, so this equals the reference's k == argmin choice);
+    // sign = parity ^ (zz_k < 0) applied as +2^31 to the bit pattern
+    const uint32_t ps = imad(__popc(nsb), K.sign, 0u);
+    const uint32_t n1s = __float_as_uint(nm1) + ps, n2s = __float_as_uint(nm2) + ps;
+    uint32_t vn = nsb;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint32_t msel = fabsf(zz[k]) == nm1 ? n2s : n1s;
+      const float lnew = __uint_as_float(imad(vn, K.sign, msel));
+      vn = imulhi(vn, K.shr);
+      msg[k] = lnew;
+      o[k] = f_add(zz[k], lnew);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// int16 row update (_kernels.py:135-170): two's-complement wrap after every
+// op.  Values are carried in 32-bit registers whose LOW 16 bits are the
+// int16 value; 16-bit shared-memory loads sign-extend and 16-bit stores
+// truncate, so the wrap after add/sub is free; |zz| and the min/max run as
+// s16x2 lane ops on the low half (abs(-32768) = -32768 sorts lowest, exactly
+// the reference's int16 behaviour).  Messages are kept as full int16 values.
+// ---------------------------------------------------------------------------
+struct ArithI16 {
+  using Val = uint32_t;
+  static constexpr int kElem = 2;
+
+  __device__ static Val lds(uint32_t a) {
+    short v; asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a)); return (uint32_t)(int)v;
+  }
+  __device__ static void sts(uint32_t a, Val v) {
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+  }
+  __device__ static bool hard(Val v) { return (int)v <= 0; }   // v is sign-extended when it comes from lds
+  __device__ static Val zero() { return 0u; }
+
+  template <int D>
+  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
+    uint32_t d[D], a[D];
+    uint32_t nsb = 0;
+    // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      d[k] = imad(msg[k], K.neg1, p[k]);                 // p - L  (FMA pipe)
+      a[k] = vmax16(d[k], imad(d[k], K.neg1, 0u));       // max(zz, -zz) in 16-bit lanes
+      add_if_neg_i16(nsb, d[k], 1u << k, K.one);
+    }
+    // min1 / min2 over a (signed int16 order), two edges per step
+    uint32_t nm1 = 0x7FFFu, nm2 = 0x7FFFu;               // 32767 (_kernels.py:142-143)
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) {
+      const uint32_t lo = vmin16(a[k], a[k + 1]), hi = vmax16(a[k], a[k + 1]);
+      nm2 = vmin16(nm2, vmin16(hi, vmax16(nm1, lo)));
+      nm1 = vmin16(nm1, lo);
+    }
+    if (D & 1) {
+      nm2 = vmin16(nm2, vmax16(nm1, a[D - 1]));
+      nm1 = vmin16(nm1, a[D - 1]);
+    }
+    // pass 2: |L_new| = nm2 iff a_k == nm1 (low halves); sign = parity ^ neg_k
+    const uint32_t par = __popc(nsb) & 1u;
+    const uint32_t n1s = par ? imad(nm1, K.neg1, 0u) : nm1;   // parity folded in
+    const uint32_t n2s = par ? imad(nm2, K.neg1, 0u) : nm2;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint32_t msel = ((a[k] ^ nm1) & 0xFFFFu) == 0u ? n2s : n1s;
+      const uint32_t lnew = (d[k] & 0x8000u) ? imad(msel, K.neg1, 0u) : msel;
+      msg[k] = lnew;
+      o[k] = imad(lnew, K.one, d[k]);                     // zz + L_new, wrapped by the 16-bit store
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// addressing
+// ---------------------------------------------------------------------------
+template <class A>
+constexpr int row_stride_bytes() { return kRowStrideUnits * A::kElem; }
+
+template <class S, class A, int ZS, int E>
+__device__ __forceinline__ uint32_t edge_addr(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+  if constexpr (ZS > 0) {
+    constexpr int sh = S::SHIFT0[E];
+    constexpr uint32_t off = (uint32_t)((sh * kRowStrideUnits + S::COL[E]) * A::kElem);
+    if constexpr (sh == 0) return b0 + off;
+    else return (r >= ZS - sh ? b1 : b0) + off;
+  } else {
+    return (r >= a.thr[E] ? b1 : b0) + (uint32_t)a.off[E];
+  }
+}
+
+template <class S, class A, int ZS, int E0, int... Ks>
+__device__ __forceinline__ void tier_addrs(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t* addr,
+                                           std::integer_sequence<int, Ks...>) {
+  ((addr[Ks] = edge_addr<S, A, ZS, E0 + Ks>(a, r, b0, b1)), ...);
+}
+
+template <class S, class A, int ZS>
+struct Layered {
+  using Val = typename A::Val;
+
+  template <int T>
+  __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
+                                              Val (&msg)[S::NE]) {
+    constexpr int D = S::DEG[T];
+    constexpr int E0 = S::START[T];
+    uint32_t addr[D];
+    Val p[D], o[D];
+    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+#pragma unroll
+    for (int k = 0; k < D; ++k) p[k] = A::lds(addr[k]);
+    A::template row<D>(p, o, msg + E0, K);
+#pragma unroll
+    for (int k = 0; k < D; ++k) A::sts(addr[k], o[k]);
+  }
+
+  template <int T>
+  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+    constexpr int D = S::DEG[T];
+    constexpr int E0 = S::START[T];
+    uint32_t addr[D];
+    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    uint32_t par = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) par ^= A::hard(A::lds(addr[k])) ? 1u : 0u;
+    return par;
+  }
+
+  template <int... Ts>
+  __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
+                                               Val (&msg)[S::NE], bool work, std::integer_sequence<int, Ts...>) {
+    ((work ? tier<Ts>(a, K, r, b0, b1, msg) : void(), __syncthreads()), ...);
+  }
+
+  template <int... Ts>
+  __device__ __forceinline__ static uint32_t parity_all(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                        std::integer_sequence<int, Ts...>) {
+    return (parity<Ts>(a, r, b0, b1) | ...);
+  }
+};
+
+// Register cap: the messages (S::NE) plus ~52 for the widest tier's
+// transients.  Measured on C2 (NE = 76): 161 regs uncapped -> 4 CTAs of 96
+// threads per SM, 45.9 Gb/s; capped at 128 -> 5 CTAs, 50.3 Gb/s; capped at
+// 96 -> spills, 43.0 Gb/s.
+#ifndef QCB_REG_SLACK
+#define QCB_REG_SLACK 52
+#endif
+// int16 keeps two values per edge of the current tier (d and |zz|): + MAXDEG
+template <class S, class A>
+constexpr int reg_cap() {
+  constexpr int want = S::NE + QCB_REG_SLACK + (A::kElem == 2 ? S::MAXDEG : 0);
+  return (want + 7) / 8 * 8 > 255 ? 255 : (want + 7) / 8 * 8;
+}
+
+template <class S, class A, int ZS, bool ET>
+__global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A>()))
+    decode_layered_kernel(const __grid_constant__ SpecArgs a) {
+  using L = Layered<S, A, ZS>;
+  using Val = typename A::Val;
+  constexpr int RS = row_stride_bytes<A>();
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_fail[kLayMaxCw], s_done[kLayMaxCw], s_iters[kLayMaxCw];
+  __shared__ int s_active;
+
+  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1};
+  const int Z = ZS > 0 ? ZS : a.z;
+  const int N = S::NB * Z;
+  const int G = a.pairs;                        // codewords per CTA
+  const int tid = threadIdx.x;
+  const int g = tid / Z, r = tid - g * Z;
+  const int64_t cw0 = (int64_t)blockIdx.x * G;
+  const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
+  const bool act = g < ncw;
+  const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);   // bytes per codeword block
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  // opaque copies keep the row bases in registers (no per-tier rematerialisation)
+  uint32_t b0 = sbase + (uint32_t)g * cws + (uint32_t)(r * RS), b1;
+  asm volatile("mov.b32 %0, %0;" : "+r"(b0));
+  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+
+  // ---- channel LLRs -> [cw][c][j] (coalesced global reads) ------------------
+  {
+    const int nthr = blockDim.x;
+    const int dj = nthr / Z, dc = nthr - dj * Z;
+    for (int q = 0; q < ncw; ++q) {
+      const uint32_t cb = sbase + (uint32_t)q * cws;
+      int j = tid / Z, c = tid - (tid / Z) * Z;
+      if constexpr (A::kElem == 4) {
+        const float* src = reinterpret_cast<const float*>(a.llr) + (cw0 + q) * N;
+        for (int n = tid; n < N; n += nthr) {
+          const float v = __ldcs(src + n);
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(cb + c * RS + j * 4), "f"(v));
+          c += dc; j += dj;
+          if (c >= Z) { c -= Z; ++j; }
+        }
+      } else {
+        const short* src = reinterpret_cast<const short*>(a.llr) + (cw0 + q) * N;
+        for (int n = tid; n < N; n += nthr) {
+          const short v = __ldcs(src + n);
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(cb + c * RS + j * 2), "h"(v));
+          c += dc; j += dj;
+          if (c >= Z) { c -= Z; ++j; }
+        }
+      }
+    }
+    for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
+      s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
+    }
+  }
+  __syncthreads();
+
+  Val msg[S::NE];
+#pragma unroll
+  for (int e = 0; e < S::NE; ++e) msg[e] = A::zero();
+
+  const auto tiers = std::make_integer_sequence<int, S::MB>{};
+  for (int k = 0; k < a.max_iters; ++k) {
+    const bool work = act && !(ET && s_done[g]);
+    L::sweep(a, K, r, b0, b1, msg, work, tiers);
+    const bool last = (k + 1 == a.max_iters);
+    if (ET || last) {                           // syndrome (_kernels.py:85-96)
+      if (tid < kLayMaxCw) s_fail[tid] = 0;
+      __syncthreads();
+      if (work && L::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
+      __syncthreads();
+    }
+    if (tid == 0) s_active = 0;
+    __syncthreads();
+    if (tid < ncw && !s_done[tid]) {
+      s_iters[tid] = k + 1;
+      if (ET && !s_fail[tid]) s_done[tid] = 1;  // converged: frozen from now on
+      else s_active = 1;
+    }
+    __syncthreads();
+    if (!s_active) break;
+  }
+
+  // ---- outputs: iterations, converged, hard decisions, posteriors -------------
+  if (tid < ncw) {
+    a.iters[cw0 + tid] = s_iters[tid];
+    a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
+  }
+  const int nthr = blockDim.x;
+  if (a.hard_packed) {
+    const int nbytes = (N + 7) >> 3;
+    uint8_t* hp = reinterpret_cast<uint8_t*>(a.hard) + cw0 * nbytes;
+    for (int i = tid; i < ncw * nbytes; i += nthr) {
+      const int q = i / nbytes, b = i - q * nbytes;
+      const uint32_t cb = sbase + (uint32_t)q * cws;
+      uint32_t byte = 0;
+      int n = b * 8;
+      int j = n / Z, c = n - j * Z;
+#pragma unroll
+      for (int u = 0; u < 8; ++u, ++n) {
+        const bool h = n < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
+        byte = (byte << 1) | (h ? 1u : 0u);
+        if (++c == Z) { c = 0; ++j; }
+      }
+      hp[i] = (uint8_t)byte;
+    }
+  } else {
+    uint8_t* h = reinterpret_cast<uint8_t*>(a.hard) + cw0 * N;
+    for (int q = 0; q < ncw; ++q) {
+      const uint32_t cb = sbase + (uint32_t)q * cws;
+      for (int n4 = tid * 4; n4 < N; n4 += nthr * 4) {
+        int j = n4 / Z, c = n4 - j * Z;
+        uint32_t word = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool hb = (n4 + u) < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
+          word |= (hb ? 1u : 0u) << (8 * u);
+          if (++c == Z) { c = 0; ++j; }
+        }
+        uint8_t* dst = h + (int64_t)q * N + n4;
+        if (n4 + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) *reinterpret_cast<uint32_t*>(dst) = word;
+        else for (int u = 0; n4 + u < N; ++u) dst[u] = (uint8_t)(word >> (8 * u));
+      }
+    }
+  }
+  if (a.post) {
+    for (int q = 0; q < ncw; ++q) {
+      const uint32_t cb = sbase + (uint32_t)q * cws;
+      for (int n = tid; n < N; n += nthr) {
+        const int j = n / Z, c = n - j * Z;
+        const Val v = A::lds(cb + c * RS + j * A::kElem);
+        if constexpr (A::kElem == 4) reinterpret_cast<float*>(a.post)[(cw0 + q) * N + n] = v;
+        else reinterpret_cast<int16_t*>(a.post)[(cw0 + q) * N + n] = (int16_t)v;
+      }
+    }
+  }
+}
+
+// codewords per CTA: whole warps, small CTAs (one barrier per tier), and
+// enough CTAs to cover every SM when the batch is small
+inline int layered_cw_per_cta(int z, int64_t w) {
+  if (const char* env = getenv("QCB_CW_PER_CTA")) {   // tuning knob (benchmarks only)
+    const int v = atoi(env);
+    if (v >= 1 && v <= kLayMaxCw && v * z <= kLayMaxThreads) return v;
+  }
+  int best = 1;
+  double best_eff = 0.0;
+  for (int p = 1; p <= kLayMaxCw; ++p) {
+    const int thr = p * z;
+    if (thr > kLayMaxThreads) break;
+    if (p > 1 && w < (int64_t)p * 148 * 4) break;   // keep >= 4 CTAs per SM on small batches
+    const int padded = (thr + 31) / 32 * 32;
+    double eff = (double)thr / padded;
+    if (thr > 160) eff *= 0.97;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = p; }
+  }
+  return best;
+}
+
+template <class S, class A, int ZS, bool ET>
+inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
+  constexpr int RS = row_stride_bytes<A>();
+  const int z = ZS > 0 ? ZS : a.z;
+  const int threads = (a.pairs * z + 31) / 32 * 32;
+  const size_t smem = (size_t)a.pairs * ((z * RS + 15) & ~15);
+  auto kern = decode_layered_kernel<S, A, ZS, ET>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
+  if (blocks <= 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace qcb

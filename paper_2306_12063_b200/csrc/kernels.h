@@ -35,18 +35,16 @@ struct SpecArgs {
   void* post;
   int64_t w;
   int32_t n, z, max_iters, early_term, hard_packed;
-  int32_t pairs;   // int16: codeword pairs per CTA; float32: codewords per CTA
-  uint32_t k_one, k_sign, k_shr;  // 1, 2^31, 2^31+1: IMAD multipliers kept out of ptxas' reach
-  int32_t zrs;     // Z * row stride (bytes)
-  int32_t ps;      // pair stride (bytes)
+  int32_t pairs;   // codewords per CTA
+  uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
   int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
 };
 
 // returns cudaErrorInvalidValue if no specialised kernel exists for (structure, elem)
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
-int spec_row_stride_bytes(int elem);   // RS for the SMEM layout (bytes per c-row)
-int spec_group_per_cta(int elem, int z);  // float32: codewords per CTA, int16: pairs per CTA
+int spec_row_stride_bytes(int elem);   // bytes per c-row of the shared-memory layout
+int spec_cw_per_cta(int z, int64_t w);
 
 // Packed direct encoder (encoder.py:166-199), byte-aligned Z.
 struct EncodeArgs {

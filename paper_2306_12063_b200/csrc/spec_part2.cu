@@ -1,24 +1,21 @@
-// spec_part2.cu -- instantiations of the specialised decoder for the
-// structures with ID % 6 == 2 (see decode_spec.cu).
-#include "decode_f32.cuh"
-#include "decode_spec.cuh"
+// spec_part2.cu -- instantiations of the layered decoder for the
+// structures with ID % 6 == 2 (see decode_spec.cu / decode_layered.cuh).
+#include "decode_layered.cuh"
 
 namespace qcb {
 
+template <class S, class A>
+static cudaError_t launch_arith(const SpecArgs& a, cudaStream_t s) {
+  if (a.z == S::Z0)
+    return a.early_term ? launch_layered<S, A, S::Z0, true>(a, s) : launch_layered<S, A, S::Z0, false>(a, s);
+  return a.early_term ? launch_layered<S, A, 0, true>(a, s) : launch_layered<S, A, 0, false>(a, s);
+}
+
 cudaError_t launch_spec_part2(int structure_id, int elem, const SpecArgs& a, cudaStream_t s) {
-#define QCB_DISPATCH(STRUCT)                                                                \
-  if constexpr (STRUCT::ID % 6 == 2) {                                                   \
-    if (structure_id == STRUCT::ID) {                                                      \
-      if (elem == 4) {                                                                    \
-        if (a.z == STRUCT::Z0)                                                            \
-          return a.early_term ? launch_f32<STRUCT, STRUCT::Z0, true>(a, s)                \
-                              : launch_f32<STRUCT, STRUCT::Z0, false>(a, s);              \
-        return a.early_term ? launch_f32<STRUCT, 0, true>(a, s)                           \
-                            : launch_f32<STRUCT, 0, false>(a, s);                         \
-      }                                                                                   \
-      return a.early_term ? launch_one<STRUCT, I16Pair, true>(a, s)                         \
-                          : launch_one<STRUCT, I16Pair, false>(a, s);                       \
-    }                                                                                      \
+#define QCB_DISPATCH(STRUCT)                                                              \
+  if constexpr (STRUCT::ID % 6 == 2) {                                                 \
+    if (structure_id == STRUCT::ID)                                                       \
+      return elem == 4 ? launch_arith<STRUCT, ArithF32>(a, s) : launch_arith<STRUCT, ArithI16>(a, s); \
   }
   QCB_FOR_EACH_STRUCTURE(QCB_DISPATCH)
 #undef QCB_DISPATCH
