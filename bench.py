@@ -323,17 +323,15 @@ def run_ours(args, wl):
     value = bits_per_step / (ms_per_step * 1e-3) / 1e9
 
     # counters (bit/frame errors vs the transmitted codewords, iterations) -> one NCCL all_reduce
-    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    from paper_2306_12063_b200 import shard
+    cnt = torch.zeros(5, dtype=torch.int64, device=dev)
     for (hard, iters, conv), pool, mm in zip(outs, pools, mms):
         w = hard.shape[0]
         for c0 in range(0, w, 1 << 16):
             c1 = min(w, c0 + (1 << 16))
             ref = pool[torch.arange(c0, c1, device=dev) % pool.shape[0]]
-            err = (hard[c0:c1, :mm.k] != ref[:, :mm.k]).sum(dim=1)
-            cnt += torch.stack([err.sum(), (err > 0).sum(), iters[c0:c1].sum().to(torch.int64),
-                                conv[c0:c1].sum().to(torch.int64)])
-    if dist:
-        dist.all_reduce(cnt)
+            cnt += shard.decode_counters(hard[c0:c1], iters[c0:c1], conv[c0:c1], ref, mm.k)
+    shard.all_reduce_counters(cnt)
     cnt = cnt.cpu().tolist()
 
     peaks, peak_kind = measured_peaks()
@@ -375,7 +373,7 @@ def run_ours(args, wl):
             "gpu_launches": args.steps * len(codes),
             "clocks": clocks.summary(),
             "counters": {"bit_errors": cnt[0], "frame_errors": cnt[1], "iter_sum": cnt[2],
-                         "converged": cnt[3], "frames": wl.w_total * world,
+                         "converged": cnt[3], "frames": cnt[4],
                          "ber": cnt[0] / max(1, wl.w_total * world * mms[0].k)},
         }
         if e2e:

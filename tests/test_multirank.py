@@ -1,0 +1,72 @@
+"""Multi-rank logic on CPU (gloo, world size 2): codeword shards cover the
+batch exactly once, per-rank counters sum to the single-process counters, and
+the per-shard work is independent of the rank count."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2306_12063_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_ranges_partition_the_batch():
+    for w in (0, 1, 7, 65536, 1 << 22):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard.shard_range(w, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == w
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard.shard_range(10, 2, 2)
+
+
+def _worker(rank, world, port, w, k, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(1234)           # identical global batch on every rank
+    hard = torch.randint(0, 2, (w, n), dtype=torch.uint8, generator=g)
+    info = torch.randint(0, 2, (w, k), dtype=torch.uint8, generator=g)
+    iters = torch.randint(1, 11, (w,), dtype=torch.int32, generator=g)
+    conv = torch.randint(0, 2, (w,), dtype=torch.uint8, generator=g)
+    a, b = shard.shard_range(w, rank, world)
+    cnt = shard.decode_counters(hard[a:b], iters[a:b], conv[a:b], info[a:b], k)
+    shard.all_reduce_counters(cnt)
+    if rank == 0:
+        q.put(cnt.tolist())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_counters_all_reduce_over_two_gloo_ranks():
+    w, k, n = 1001, 48, 96
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, w, k, n, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = torch.Generator().manual_seed(1234)
+    hard = torch.randint(0, 2, (w, n), dtype=torch.uint8, generator=g)
+    info = torch.randint(0, 2, (w, k), dtype=torch.uint8, generator=g)
+    iters = torch.randint(1, 11, (w,), dtype=torch.int32, generator=g)
+    conv = torch.randint(0, 2, (w,), dtype=torch.uint8, generator=g)
+    want = shard.decode_counters(hard, iters, conv, info, k).tolist()
+    assert got == want and got[4] == w
