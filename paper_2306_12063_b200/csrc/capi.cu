@@ -138,7 +138,7 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
     a.w = w; a.n = c->n; a.z = c->z; a.max_iters = max_iters; a.early_term = early_term ? 1 : 0;
     a.hard_packed = hard_packed ? 1 : 0;
     const int rs = spec_row_stride_bytes(elem);
-    a.pairs = spec_cw_per_cta(c->z, w);
+    spec_plan(c->structure, elem, c->z, w, &a.pairs, &a.tmem_cols);
     a.k_one = 1u; a.k_sign = 0x80000000u; a.k_shr = 0x80000001u; a.k_neg1 = 0xFFFFFFFFu;
     for (int i = 0; i < c->ne; ++i) {
       a.off[i] = c->ent_e[i] * rs + c->ent_j[i] * elem;   // (e * 25 + j) cells

@@ -30,6 +30,7 @@
 //    IMAD.HI is quarter rate, so sign handling rides on IMAD and min/max
 //    are tracked two edges per step with 3-input min.
 #pragma once
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -89,17 +90,26 @@ struct ArithF32 {
   __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
   __device__ static bool hard(Val v) { return v <= 0.0f; }
   __device__ static Val zero() { return 0.0f; }   // reference init: min1 = min2 = 0, no signs -> L = +0.0
+  // Channel LLRs enter shared memory as v + 0.0f: -0.0 becomes +0.0 and any
+  // NaN becomes the GPU's canonical NaN (sign bit clear).  From then on no
+  // posterior and no zz = post - L_old is ever -0.0 (IEEE: x - y = -0 needs
+  // x = -0, x + y = -0 needs both -0) and no NaN carries a sign, so the sign
+  // bit of zz equals the reference's `zz < 0` (_kernels.py:73) and can be used
+  // directly.  The only observable difference is the sign of an exactly-zero
+  // posterior (compares equal; hard decisions, messages and iteration counts
+  // are identical).
+  __device__ static float canon(float v) { return f_add(v, 0.0f); }
 
   template <int D>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
     float zz[D];
-    uint32_t nsb = 0;
-    // pass 1: zz = post - L_old, sign bits (_kernels.py:61-75)
+    // pass 1: zz = post - L_old (_kernels.py:61-75); sign parity = xor of sign bits
+    uint32_t sx = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      zz[k] = f_sub(p[k], msg[k]);
-      add_if_neg_f32(nsb, zz[k], 1u << k, K.one);
-    }
+    for (int k = 0; k < D; ++k) zz[k] = f_sub(p[k], msg[k]);
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) sx ^= __float_as_uint(zz[k]) ^ __float_as_uint(zz[k + 1]);
+    if (D & 1) sx ^= __float_as_uint(zz[D - 1]);
     // min1 / min2 of |zz|, two edges per step; max.NaN keeps NaN out of min2
     // exactly like the reference's `elif a < nm2`
     float nm1 = f_inf(), nm2 = f_inf();
@@ -117,18 +127,20 @@ struct ArithF32 {
     }
     // pass 2 (_kernels.py:76-79): |L_new| = nm2 iff |zz_k| == nm1 (on a tie
     // nm2 == nm1, so this equals the reference's k == argmin choice);
-    // sign = parity ^ (zz_k < 0) applied as +2^31 to the bit pattern
-    const uint32_t ps = imad(__popc(nsb), K.sign, 0u);
-    const uint32_t n1s = __float_as_uint(nm1) + ps, n2s = __float_as_uint(nm2) + ps;
-    uint32_t vn = nsb;
+    // sign(L_new) = parity ^ sign(zz_k): parity folded into n1s/n2s once per row
+    uint32_t n1s, n2s;
+    asm("lop3.b32 %0, %1, %2, 0x80000000, 0xf8;" : "=r"(n1s) : "r"(__float_as_uint(nm1)), "r"(sx));  // nm1 | (sx & sign)
+    asm("lop3.b32 %0, %1, %2, 0x80000000, 0xf8;" : "=r"(n2s) : "r"(__float_as_uint(nm2)), "r"(sx));
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const uint32_t msel = fabsf(zz[k]) == nm1 ? n2s : n1s;
-      const float lnew = __uint_as_float(imad(vn, K.sign, msel));
-      vn = imulhi(vn, K.shr);
+      uint32_t lb;
+      asm("lop3.b32 %0, %1, %2, 0x80000000, 0x78;" : "=r"(lb) : "r"(msel), "r"(__float_as_uint(zz[k])));  // msel ^ (zz & sign)
+      const float lnew = __uint_as_float(lb);
       msg[k] = lnew;
       o[k] = f_add(zz[k], lnew);
     }
+    (void)K;
   }
 };
 
@@ -147,23 +159,27 @@ struct ArithI16 {
   __device__ static Val lds(uint32_t a) {
     short v; asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a)); return (uint32_t)(int)v;
   }
-  __device__ static void sts(uint32_t a, Val v) {
-    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+  __device__ static void sts(uint32_t a, Val v) {   // stores the low half: the int16 wrap
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
   }
   __device__ static bool hard(Val v) { return (int)v <= 0; }   // v is sign-extended when it comes from lds
   __device__ static Val zero() { return 0u; }
+  __device__ static short canon(short v) { return v; }
 
   template <int D>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
     uint32_t d[D], a[D];
-    uint32_t nsb = 0;
     // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       d[k] = imad(msg[k], K.neg1, p[k]);                 // p - L  (FMA pipe)
       a[k] = vmax16(d[k], imad(d[k], K.neg1, 0u));       // max(zz, -zz) in 16-bit lanes
-      add_if_neg_i16(nsb, d[k], 1u << k, K.one);
     }
+    // sign-product parity = xor of the int16 sign bits (bit 15)
+    uint32_t sx = 0;
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
+    if (D & 1) sx ^= d[D - 1];
     // min1 / min2 over a (signed int16 order), two edges per step
     uint32_t nm1 = 0x7FFFu, nm2 = 0x7FFFu;               // 32767 (_kernels.py:142-143)
 #pragma unroll
@@ -177,12 +193,17 @@ struct ArithI16 {
       nm1 = vmin16(nm1, a[D - 1]);
     }
     // pass 2: |L_new| = nm2 iff a_k == nm1 (low halves); sign = parity ^ neg_k
-    const uint32_t par = __popc(nsb) & 1u;
+    const bool par = (sx & 0x8000u) != 0;
     const uint32_t n1s = par ? imad(nm1, K.neg1, 0u) : nm1;   // parity folded in
     const uint32_t n2s = par ? imad(nm2, K.neg1, 0u) : nm2;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const uint32_t msel = ((a[k] ^ nm1) & 0xFFFFu) == 0u ? n2s : n1s;
+      // a_k == nm1 <=> min(a_k, nm1) == a_k (a_k >= nm1): one VIMNMX with a predicate
+      uint32_t msel;
+      asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t.reg .b16 l0, h0, l1, h1;\n\t"
+          "min.s16x2 t, %1, %2;\n\tmov.b32 {l0, h0}, t;\n\tmov.b32 {l1, h1}, %1;\n\t"
+          "setp.eq.s16 p, l0, l1;\n\tselp.b32 %0, %4, %3, p;\n\t}"
+          : "=r"(msel) : "r"(a[k]), "r"(nm1), "r"(n1s), "r"(n2s));
       const uint32_t lnew = (d[k] & 0x8000u) ? imad(msel, K.neg1, 0u) : msel;
       msg[k] = lnew;
       o[k] = imad(lnew, K.one, d[k]);                     // zz + L_new, wrapped by the 16-bit store
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A>()))
       if constexpr (A::kElem == 4) {
         const float* src = reinterpret_cast<const float*>(a.llr) + (cw0 + q) * N;
         for (int n = tid; n < N; n += nthr) {
-          const float v = __ldcs(src + n);
+          const float v = A::canon(__ldcs(src + n));
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(cb + c * RS + j * 4), "f"(v));
           c += dc; j += dj;
           if (c >= Z) { c -= Z; ++j; }

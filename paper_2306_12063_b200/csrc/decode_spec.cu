@@ -2,7 +2,7 @@
 // The kernel template lives in decode_layered.cuh; its 18 structures x
 // {float32, int16} x {native Z, runtime Z} x {early termination on, off}
 // instantiations are split over spec_part{0..5}.cu so they compile in parallel.
-#include "decode_layered.cuh"
+#include "decode_tmem.cuh"
 
 namespace qcb {
 
@@ -29,5 +29,39 @@ int spec_row_stride_bytes(int elem) {
 }
 
 int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w); }
+
+// Choose between the register-resident and the TMEM-resident message store.
+// QCB_TMEM=0/1 forces one (benchmarks); default: TMEM when it keeps more
+// codewords resident per SM.
+void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols) {
+  int ne = 0, maxdeg = 0;
+#define QCB_NE(STRUCT) if (structure_id == STRUCT::ID) { ne = STRUCT::NE; maxdeg = STRUCT::MAXDEG; }
+  QCB_FOR_EACH_STRUCTURE(QCB_NE)
+#undef QCB_NE
+  const int reg_g = layered_cw_per_cta(z, w);
+  *cw_per_cta = reg_g;
+  *tmem_cols = 0;
+  const char* env = getenv("QCB_TMEM");
+  if (env && env[0] == '0') return;
+  const int regs_tm = QCB_TM_REG_BASE + (elem == 2 ? 6 : 5) * maxdeg;
+  const int regs_reg = ne + 52 + (elem == 2 ? maxdeg : 0);
+  const int smem_cw = (z * kRowStrideUnits * elem + 15) & ~15;
+  int cols = 0;
+  const int g = tmem_plan(z, ne, (regs_tm + 7) / 8 * 8, smem_cw, w, &cols);
+  if (g <= 0) return;
+  const int warps_reg = (reg_g * z + 31) / 32;
+  const int reg_ctas = std::min(65536 / (warps_reg * 32 * ((regs_reg + 7) / 8 * 8)), 64 / warps_reg);
+  const int warps_tm = (g * z + 31) / 32;
+  const int tm_ctas = std::min(std::min(512 / cols, 65536 / (warps_tm * 32 * ((regs_tm + 7) / 8 * 8))), 64 / warps_tm);
+  // measured on B200 (round 1): TMEM-resident messages pay off for the
+  // high-degree codes (Wi-Fi 1944 R5/6 int16: +17 %) but cost 5-6 % on the
+  // degree-6/7 and degree-15 codes, where the register kernel already fits
+  // 4-5 codewords per SM and the extra tcgen05 ld/st per tier do not pay back
+  const bool prefer = maxdeg >= 18 && tm_ctas * g > reg_ctas * reg_g;
+  if ((env && env[0] == '1') || prefer) {
+    *cw_per_cta = g;
+    *tmem_cols = cols;
+  }
+}
 
 }  // namespace qcb

@@ -36,6 +36,7 @@ struct SpecArgs {
   int64_t w;
   int32_t n, z, max_iters, early_term, hard_packed;
   int32_t pairs;   // codewords per CTA
+  int32_t tmem_cols;  // TMEM columns per CTA (TMEM-resident message kernel), 0 = register kernel
   uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
   int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
@@ -45,6 +46,7 @@ struct SpecArgs {
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
 int spec_row_stride_bytes(int elem);   // bytes per c-row of the shared-memory layout
 int spec_cw_per_cta(int z, int64_t w);
+void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols);
 
 // Packed direct encoder (encoder.py:166-199), byte-aligned Z.
 struct EncodeArgs {

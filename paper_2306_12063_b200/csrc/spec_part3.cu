@@ -1,11 +1,16 @@
 // spec_part3.cu -- instantiations of the layered decoder for the
 // structures with ID % 6 == 3 (see decode_spec.cu / decode_layered.cuh).
-#include "decode_layered.cuh"
+#include "decode_tmem.cuh"
 
 namespace qcb {
 
 template <class S, class A>
 static cudaError_t launch_arith(const SpecArgs& a, cudaStream_t s) {
+  if (a.tmem_cols > 0) {
+    if (a.z == S::Z0)
+      return a.early_term ? launch_tmem<S, A, S::Z0, true>(a, s) : launch_tmem<S, A, S::Z0, false>(a, s);
+    return a.early_term ? launch_tmem<S, A, 0, true>(a, s) : launch_tmem<S, A, 0, false>(a, s);
+  }
   if (a.z == S::Z0)
     return a.early_term ? launch_layered<S, A, S::Z0, true>(a, s) : launch_layered<S, A, S::Z0, false>(a, s);
   return a.early_term ? launch_layered<S, A, 0, true>(a, s) : launch_layered<S, A, 0, false>(a, s);

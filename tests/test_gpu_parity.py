@@ -37,6 +37,18 @@ def _bits(a):
     return a.view(np.uint32 if a.dtype == np.float32 else np.uint16)
 
 
+def _post_equal(got, want):
+    """int16: bitwise.  float32: bitwise except the sign of an exact zero and
+    NaN payloads -- the specialised kernel canonicalises -0.0 inputs to +0.0
+    (see ArithF32::canon in csrc/decode_layered.cuh), which can flip the sign
+    of a zero posterior; values compare equal and every decision is identical.
+    north_star allows 1e-5 relative for float posteriors."""
+    got, want = np.asarray(got), np.asarray(want)
+    if got.dtype == np.int16:
+        return np.array_equal(got, want)
+    return np.array_equal(got, want, equal_nan=True)
+
+
 def _gpu(mm, llr, cfg, posteriors=True, hard_packed=False):
     out = P.decode_batch(mm, torch.from_numpy(llr).cuda(), cfg, posteriors=posteriors,
                          hard_packed=hard_packed)
@@ -53,7 +65,7 @@ def test_device_path_matches_reference_goldens(name):
     assert np.array_equal(conv, d["conv"])
     if "post" in d:
         k = d["post"].shape[0]
-        assert np.array_equal(_bits(post[:k]), _bits(d["post"]))
+        assert _post_equal(post[:k], d["post"])
     hp, _, _ = _gpu(d["mm"], d["llr"], _cfg(d), posteriors=False, hard_packed=True)
     assert np.array_equal(hp, d["hard_packed"])
 
@@ -104,7 +116,7 @@ def test_all_126_codes_match_oracle(fixed, early):
         oh, oi, oc, op = O.decode_batch(h, llr, iters, early, workers=4, want_post=True)
         assert np.array_equal(hard, oh), (std, n, rate)
         assert np.array_equal(it, oi) and np.array_equal(conv, oc), (std, n, rate)
-        assert np.array_equal(_bits(post), _bits(op)), (std, n, rate)
+        assert _post_equal(post, op), (std, n, rate)
 
 
 def test_generic_kernel_on_nonstandard_codes():
@@ -130,7 +142,7 @@ def test_generic_kernel_on_nonstandard_codes():
                 hard, it, conv, post = _gpu(mm, llr, cfg)
                 oh, oi, oc, op = O.decode_batch(h, llr, iters, early, want_post=True)
                 assert np.array_equal(hard, oh) and np.array_equal(it, oi) and np.array_equal(conv, oc)
-                assert np.array_equal(_bits(post), _bits(op))
+                assert _post_equal(post, op)
 
 
 def test_known_answers(golden_dir):
@@ -232,7 +244,7 @@ def test_full_size_batch_properties(config):
     sample = np.random.default_rng(0).choice(4096, 512, replace=False)
     oh, oi, oc, op = O.decode_batch(h, base[sample], iters, False, want_post=True)
     assert np.array_equal(hard[sample], oh) and np.array_equal(conv[sample], oc)
-    assert np.array_equal(_bits(post[sample]), _bits(op))
+    assert _post_equal(post[sample], op)
     par = P.row_parities(h, hard[:2048])
     assert np.array_equal(conv[:2048] == 1, ~par.any(axis=-1))
 
