@@ -75,6 +75,18 @@ __device__ __forceinline__ uint32_t vmax16(uint32_t a, uint32_t b) {
   uint32_t d; asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
 }
 
+// packed float32x2 add/sub (FADD2: two IEEE float32 ops in one instruction)
+__device__ __forceinline__ void f_sub2(float a0, float a1, float b0, float b1, float& r0, float& r1) {
+  asm("{\n\t.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+      "sub.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;\n\t}"
+      : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void f_add2(float a0, float a1, float b0, float b1, float& r0, float& r1) {
+  asm("{\n\t.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+      "add.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;\n\t}"
+      : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 struct RtK {              // runtime constants (kernel parameters)
   uint32_t one, sign, shr, neg1;
 };
@@ -106,7 +118,8 @@ struct ArithF32 {
     // pass 1: zz = post - L_old (_kernels.py:61-75); sign parity = xor of sign bits
     uint32_t sx = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) zz[k] = f_sub(p[k], msg[k]);
+    for (int k = 0; k + 1 < D; k += 2) f_sub2(p[k], p[k + 1], msg[k], msg[k + 1], zz[k], zz[k + 1]);
+    if (D & 1) zz[D - 1] = f_sub(p[D - 1], msg[D - 1]);
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= __float_as_uint(zz[k]) ^ __float_as_uint(zz[k + 1]);
     if (D & 1) sx ^= __float_as_uint(zz[D - 1]);
@@ -136,10 +149,11 @@ struct ArithF32 {
       const uint32_t msel = fabsf(zz[k]) == nm1 ? n2s : n1s;
       uint32_t lb;
       asm("lop3.b32 %0, %1, %2, 0x80000000, 0x78;" : "=r"(lb) : "r"(msel), "r"(__float_as_uint(zz[k])));  // msel ^ (zz & sign)
-      const float lnew = __uint_as_float(lb);
-      msg[k] = lnew;
-      o[k] = f_add(zz[k], lnew);
+      msg[k] = __uint_as_float(lb);
     }
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) f_add2(zz[k], zz[k + 1], msg[k], msg[k + 1], o[k], o[k + 1]);
+    if (D & 1) o[D - 1] = f_add(zz[D - 1], msg[D - 1]);
     (void)K;
   }
 };
@@ -266,10 +280,17 @@ struct Layered {
     return par;
   }
 
-  template <int... Ts>
+  // without early termination every thread runs every tier (threads beyond
+  // the batch work on scratch / unused slots): no branch around the tier body
+  template <bool ET, int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
                                                Val (&msg)[S::NE], bool work, std::integer_sequence<int, Ts...>) {
-    ((work ? tier<Ts>(a, K, r, b0, b1, msg) : void(), __syncthreads()), ...);
+    if constexpr (ET) {
+      ((work ? tier<Ts>(a, K, r, b0, b1, msg) : void(), __syncthreads()), ...);
+    } else {
+      (void)work;
+      ((tier<Ts>(a, K, r, b0, b1, msg), __syncthreads()), ...);
+    }
   }
 
   template <int... Ts>
@@ -314,8 +335,10 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A>()))
   const bool act = g < ncw;
   const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);   // bytes per codeword block
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  // padding threads of the last warp (g >= G) use the scratch slot G
+  const int gs = g < G ? g : G, rs = g < G ? r : (tid - G * Z) % Z;
   // opaque copies keep the row bases in registers (no per-tier rematerialisation)
-  uint32_t b0 = sbase + (uint32_t)g * cws + (uint32_t)(r * RS), b1;
+  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
 
@@ -357,12 +380,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A>()))
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   for (int k = 0; k < a.max_iters; ++k) {
     const bool work = act && !(ET && s_done[g]);
-    L::sweep(a, K, r, b0, b1, msg, work, tiers);
+    L::template sweep<ET>(a, K, rs, b0, b1, msg, work, tiers);
     const bool last = (k + 1 == a.max_iters);
     if (ET || last) {                           // syndrome (_kernels.py:85-96)
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (work && L::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
+      if (work && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
       __syncthreads();
     }
     if (tid == 0) s_active = 0;
@@ -457,7 +480,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   constexpr int RS = row_stride_bytes<A>();
   const int z = ZS > 0 ? ZS : a.z;
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)a.pairs * ((z * RS + 15) & ~15);
+  const size_t smem = (size_t)(a.pairs + 1) * ((z * RS + 15) & ~15);   // + scratch slot
   auto kern = decode_layered_kernel<S, A, ZS, ET>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
