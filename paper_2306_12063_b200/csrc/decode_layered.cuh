@@ -112,49 +112,52 @@ struct ArithF32 {
   // are identical).
   __device__ static float canon(float v) { return f_add(v, 0.0f); }
 
+  // Leave-one-out formulation: |L_new_k| = min_{j != k} |zz_j| (prefix and
+  // suffix minima).  This is the reference's (k == argmin ? min2 : min1)
+  // exactly: for k != argmin the minimum over j != k still contains min1; for
+  // k == argmin it is the second smallest with multiplicity (= min2, ties
+  // included).  NaN |zz| never wins (fminf ignores NaN, as the reference's
+  // `a < nm1` / `a < nm2` do) and the chains are seeded with +inf, the
+  // reference's initial min1 / min2.  3*D - 6 min instructions per row
+  // instead of ~2.1*D for min1/min2 plus 2*D for the per-edge min1/min2 pick.
   template <int D>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
+    static_assert(D >= 2, "row degree >= 2");
     float zz[D];
     // pass 1: zz = post - L_old (_kernels.py:61-75); sign parity = xor of sign bits
-    uint32_t sx = 0;
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) f_sub2(p[k], p[k + 1], msg[k], msg[k + 1], zz[k], zz[k + 1]);
     if (D & 1) zz[D - 1] = f_sub(p[D - 1], msg[D - 1]);
+    uint32_t sx = 0;
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= __float_as_uint(zz[k]) ^ __float_as_uint(zz[k + 1]);
     if (D & 1) sx ^= __float_as_uint(zz[D - 1]);
-    // min1 / min2 of |zz|, two edges per step; max.NaN keeps NaN out of min2
-    // exactly like the reference's `elif a < nm2`
-    float nm1 = f_inf(), nm2 = f_inf();
+    const uint32_t sxm = sx & 0x80000000u;
+    // leave-one-out minima of |zz|
+    float pre[D], suf[D], ex[D];
+    pre[1] = fabsf(zz[0]);
 #pragma unroll
-    for (int k = 0; k + 1 < D; k += 2) {
-      const float x = fabsf(zz[k]), y = fabsf(zz[k + 1]);
-      const float lo = fminf(x, y), hi = f_max_nan(x, y);
-      nm2 = fminf(nm2, fminf(hi, f_max_nan(nm1, lo)));
-      nm1 = fminf(nm1, lo);
-    }
-    if (D & 1) {
-      const float x = fabsf(zz[D - 1]);
-      nm2 = fminf(nm2, f_max_nan(nm1, x));
-      nm1 = fminf(nm1, x);
-    }
-    // pass 2 (_kernels.py:76-79): |L_new| = nm2 iff |zz_k| == nm1 (on a tie
-    // nm2 == nm1, so this equals the reference's k == argmin choice);
-    // sign(L_new) = parity ^ sign(zz_k): parity folded into n1s/n2s once per row
-    uint32_t n1s, n2s;
-    asm("lop3.b32 %0, %1, %2, 0x80000000, 0xf8;" : "=r"(n1s) : "r"(__float_as_uint(nm1)), "r"(sx));  // nm1 | (sx & sign)
-    asm("lop3.b32 %0, %1, %2, 0x80000000, 0xf8;" : "=r"(n2s) : "r"(__float_as_uint(nm2)), "r"(sx));
+    for (int k = 2; k < D; ++k) pre[k] = k == 2 ? fminf(fminf(fabsf(zz[0]), fabsf(zz[1])), f_inf())
+                                               : fminf(pre[k - 1], fabsf(zz[k - 1]));
+    suf[D - 2] = fabsf(zz[D - 1]);
+#pragma unroll
+    for (int k = D - 3; k >= 0; --k) suf[k] = k == D - 3 ? fminf(fminf(fabsf(zz[D - 1]), fabsf(zz[D - 2])), f_inf())
+                                                          : fminf(suf[k + 1], fabsf(zz[k + 1]));
+    ex[0] = D == 2 ? fminf(suf[0], f_inf()) : suf[0];
+    ex[D - 1] = D == 2 ? fminf(pre[D - 1], f_inf()) : pre[D - 1];
+#pragma unroll
+    for (int k = 1; k < D - 1; ++k) ex[k] = fminf(pre[k], suf[k]);
+    // pass 2 (_kernels.py:76-79): L_new = +-ex, sign = parity ^ sign(zz_k);
+    // ex >= 0, so the sign is added to the bit pattern (IMAD, FMA pipe)
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const uint32_t msel = fabsf(zz[k]) == nm1 ? n2s : n1s;
-      uint32_t lb;
-      asm("lop3.b32 %0, %1, %2, 0x80000000, 0x78;" : "=r"(lb) : "r"(msel), "r"(__float_as_uint(zz[k])));  // msel ^ (zz & sign)
-      msg[k] = __uint_as_float(lb);
+      uint32_t t;
+      asm("lop3.b32 %0, %1, %2, 0x80000000, 0x28;" : "=r"(t) : "r"(__float_as_uint(zz[k])), "r"(sxm));  // (zz ^ sxm) & sign
+      msg[k] = __uint_as_float(imad(t, K.one, __float_as_uint(ex[k])));
     }
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) f_add2(zz[k], zz[k + 1], msg[k], msg[k + 1], o[k], o[k + 1]);
     if (D & 1) o[D - 1] = f_add(zz[D - 1], msg[D - 1]);
-    (void)K;
   }
 };
 
@@ -166,6 +169,11 @@ struct ArithF32 {
 // s16x2 lane ops on the low half (abs(-32768) = -32768 sorts lowest, exactly
 // the reference's int16 behaviour).  Messages are kept as full int16 values.
 // ---------------------------------------------------------------------------
+#ifndef QCB_I16_LOO_MAXDEG
+#define QCB_I16_LOO_MAXDEG 10
+#endif
+constexpr int kI16LooMaxDeg = QCB_I16_LOO_MAXDEG;
+
 struct ArithI16 {
   using Val = uint32_t;
   static constexpr int kElem = 2;
@@ -180,8 +188,10 @@ struct ArithI16 {
   __device__ static Val zero() { return 0u; }
   __device__ static short canon(short v) { return v; }
 
+  // min1/min2 pair formulation (fewer live values than leave-one-out: used
+  // for high-degree rows, where the leave-one-out arrays would spill)
   template <int D>
-  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
+  __device__ __forceinline__ static void row_pair(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
     uint32_t d[D], a[D];
     // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
 #pragma unroll
@@ -221,6 +231,52 @@ struct ArithI16 {
       const uint32_t lnew = (d[k] & 0x8000u) ? imad(msel, K.neg1, 0u) : msel;
       msg[k] = lnew;
       o[k] = imad(lnew, K.one, d[k]);                     // zz + L_new, wrapped by the 16-bit store
+    }
+  }
+
+  // Leave-one-out formulation as for float32: |L_new_k| = min_{j != k} a_j in
+  // signed int16 order (abs(-32768) = -32768 sorts lowest, as in the
+  // reference); equals the reference's (k == argmin ? min2 : min1).
+  template <int D>
+  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
+    if constexpr (D > kI16LooMaxDeg) {
+      row_pair<D>(p, o, msg, K);
+      return;
+    }
+    static_assert(D >= 2, "row degree >= 2");
+    uint32_t d[D], a[D];
+    // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      d[k] = imad(msg[k], K.neg1, p[k]);                 // p - L  (FMA pipe)
+      a[k] = vmax16(d[k], imad(d[k], K.neg1, 0u));       // max(zz, -zz) in 16-bit lanes
+    }
+    // sign-product parity = xor of the int16 sign bits (bit 15)
+    uint32_t sx = 0;
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
+    if (D & 1) sx ^= d[D - 1];
+    // leave-one-out minima (low halves; 32767 = the reference's initial min)
+    uint32_t pre[D], suf[D], ex[D];
+    pre[1] = a[0];
+#pragma unroll
+    for (int k = 2; k < D; ++k) pre[k] = vmin16(pre[k - 1], a[k - 1]);
+    suf[D - 2] = a[D - 1];
+#pragma unroll
+    for (int k = D - 3; k >= 0; --k) suf[k] = vmin16(suf[k + 1], a[k + 1]);
+    ex[0] = suf[0];
+    ex[D - 1] = pre[D - 1];
+#pragma unroll
+    for (int k = 1; k < D - 1; ++k) ex[k] = vmin16(pre[k], suf[k]);
+    // pass 2: L_new = +-ex with sign = parity ^ (zz_k < 0): sigma = +-1 from
+    // bit 15 of (d ^ sx); msg = ex * sigma, post = d + ex * sigma (both IMAD)
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      uint32_t sg;
+      asm("{\n\t.reg .b32 t;\n\txor.b32 t, %1, %2;\n\tprmt.b32 t, t, 0, 0x9999;\n\tor.b32 %0, t, 1;\n\t}"
+          : "=r"(sg) : "r"(d[k]), "r"(sx));
+      msg[k] = imad(ex[k], sg, 0u);
+      o[k] = imad(ex[k], sg, d[k]);                       // zz + L_new, wrapped by the 16-bit store
     }
   }
 };
@@ -307,15 +363,48 @@ struct Layered {
 #ifndef QCB_REG_SLACK
 #define QCB_REG_SLACK 52
 #endif
-// int16 keeps two values per edge of the current tier (d and |zz|): + MAXDEG
-template <class S, class A>
+// codewords per CTA for a large batch: whole warps, small CTAs (one barrier
+// per tier).  The host uses the same rule (layered_cw_per_cta) and only
+// shrinks G further for small batches.
+constexpr int cw_per_cta_large(int z) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int p = 1; p <= kLayMaxCw; ++p) {
+    const int thr = p * z;
+    if (thr > kLayMaxThreads) break;
+    const int padded = (thr + 31) / 32 * 32;
+    double eff = (double)thr / padded;
+    if (thr > 160) eff *= 0.97;
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = p; }
+  }
+  return best;
+}
+
+// Register cap: the messages (S::NE) plus a slack for the widest tier's
+// transients and hoisted edge addresses, then raised to the largest value that
+// still gives the same number of resident CTAs for the code's CTA size (for
+// Z = 96: 136 keeps 5 CTAs of 96 threads, 168 keeps 4).  Measured on C2
+// (NE = 76): uncapped 161 regs -> 4 CTAs, 45.9 Gb/s; 128 -> 5 CTAs, 50.3.
+template <class S, class A, int ZS>
 constexpr int reg_cap() {
-  constexpr int want = S::NE + QCB_REG_SLACK + (A::kElem == 2 ? S::MAXDEG : 0);
-  return (want + 7) / 8 * 8 > 255 ? 255 : (want + 7) / 8 * 8;
+  const int want = S::NE + QCB_REG_SLACK + (A::kElem == 2 ? S::MAXDEG : 0);
+  const int z = ZS > 0 ? ZS : 96;
+  const int threads = (cw_per_cta_large(z) * z + 31) / 32 * 32;
+  int ctas = 65536 / (threads * want);
+  if (ctas < 1) ctas = 1;
+  // measured (B200, same box, A/B): raising helps int16 (C5: 40.7 -> 43.9
+  // Gb/s at 168 regs) but hurts float32 (C2: 75.6 at 128 -> 67.3 at 136,
+  // same CTA count), so only int16 is raised
+  int cap = (want + 7) / 8 * 8;
+  if (A::kElem == 2) {
+    cap = 65536 / (threads * ctas) / 8 * 8;
+    if (cap < want) cap = (want + 7) / 8 * 8;
+  }
+  return cap > 255 ? 255 : cap;
 }
 
 template <class S, class A, int ZS, bool ET>
-__global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A>()))
+__global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>()))
     decode_layered_kernel(const __grid_constant__ SpecArgs a) {
   using L = Layered<S, A, ZS>;
   using Val = typename A::Val;
