@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    ap.add_argument("--no-encode", action="store_true", help="C5: skip the packed-encoder measurement")
     return ap.parse_args()
 
 
@@ -346,6 +347,12 @@ def run_ours(args, wl):
     if not args.no_e2e and not args.profile:
         e2e = run_e2e(args, wl, mms, llrs, world, dist, dev)
 
+    enc = None
+    if wl.key == "C5" and not args.no_encode:
+        del llrs, outs
+        torch.cuda.empty_cache()
+        enc = run_encode(args, wl, mms[0], dev, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         threads = os.cpu_count() or 1
@@ -378,12 +385,61 @@ def run_ours(args, wl):
         }
         if e2e:
             line["e2e"] = e2e
+        if enc:
+            line["encode"] = enc
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_encode(args, wl, mm, dev, dist):
+    """BASELINE config 5, second half: bit-packed direct encoding of 2^22 seeded
+    info words (K = 1728 bits) on the GPU; HBM-bound (216 B in + 288 B out per
+    codeword).  A sample is checked against the CPU oracle."""
+    import torch
+    import paper_2306_12063_b200 as P
+    plan = P.make_plan(mm, P.EncoderVariant.Packed)
+    w = wl.w_per_code
+    g = torch.Generator(device=dev).manual_seed(wl.seed * 7919)
+    info = torch.randint(0, 256, (w, mm.k // 8), dtype=torch.uint8, device=dev, generator=g)
+    stream = torch.cuda.Stream(dev)
+    out = None
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            out = P.encode_packed(plan, info, stream=stream)
+    torch.cuda.synchronize(dev)
+    steps = max(5, args.steps)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(steps):
+            out = P.encode_packed(plan, info, stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    nbytes = w * (mm.k // 8 + mm.n // 8)
+    peaks, kind = measured_peaks()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    from oracle import oracle as O
+    idx = torch.randint(0, w, (1024,), device=dev, generator=g)
+    ok = bool(np.array_equal(out[idx].cpu().numpy(), O.encode_packed(mm, info[idx].cpu().numpy())))
+    return {"metric": "encoded coded Gbit/s (C5, 2^22 x K=1728 info words)",
+            "value": round(w * mm.n * world / (ms * 1e-3) / 1e9, 2), "unit": "Gbit/s",
+            "ms_per_step": round(ms, 4), "codewords_per_gpu": w, "gpu_launches": steps,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks.get("hbm_gbs"),
+                         "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs", 6650.0), 4),
+                         "note": f"{mm.k // 8} B in + {mm.n // 8} B out per codeword ({kind} peak)"},
+            "sample_vs_oracle": "bit-exact" if ok else "MISMATCH"}
 
 
 def run_e2e(args, wl, mms, llrs, world, dist, dev):

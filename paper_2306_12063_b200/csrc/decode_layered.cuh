@@ -564,6 +564,18 @@ inline int layered_cw_per_cta(int z, int64_t w) {
   return best;
 }
 
+template <class K>
+inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s) {
+  const int threads = (a.pairs * z + 31) / 32 * 32;
+  const size_t smem = (size_t)(a.pairs + 1) * ((z * rs + 15) & ~15);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
+  if (blocks <= 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <class S, class A, int ZS, bool ET>
 inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   constexpr int RS = row_stride_bytes<A>();
@@ -573,10 +585,21 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   auto kern = decode_layered_kernel<S, A, ZS, ET>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
-  if (blocks <= 0) return cudaSuccess;
-  kern<<<(unsigned)blocks, threads, smem, s>>>(a);
-  return cudaGetLastError();
+  // the register count is only known after ptxas: shrink the CTA if this
+  // kernel cannot launch the planned one (the decode result does not depend
+  // on the CTA size)
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  if (threads > fa.maxThreadsPerBlock) {
+    SpecArgs b = a;
+    b.pairs = fa.maxThreadsPerBlock / z;
+    if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
+    if (b.tmem_cols > 0) return cudaErrorLaunchOutOfResources;   // TMEM plan is per CTA shape
+    return launch_layered_fixed(kern, b, z, RS, s);
+  }
+  return launch_layered_fixed(kern, a, z, RS, s);
 }
+
 
 }  // namespace qcb

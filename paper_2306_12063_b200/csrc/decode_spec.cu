@@ -33,6 +33,18 @@ int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w); }
 // Choose between the register-resident and the TMEM-resident message store.
 // QCB_TMEM=0/1 forces one (benchmarks); default: TMEM when it keeps more
 // codewords resident per SM.
+bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne) {
+  bool native = false;
+#define QCB_NAT(STRUCT)                                                   \
+  if (structure_id == STRUCT::ID && z == STRUCT::Z0 && ne == STRUCT::NE) { \
+    native = true;                                                        \
+    for (int i = 0; i < ne; ++i) native = native && ent_e[i] == STRUCT::SHIFT0[i]; \
+  }
+  QCB_FOR_EACH_STRUCTURE(QCB_NAT)
+#undef QCB_NAT
+  return native;
+}
+
 void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols) {
   int ne = 0, maxdeg = 0;
 #define QCB_NE(STRUCT) if (structure_id == STRUCT::ID) { ne = STRUCT::NE; maxdeg = STRUCT::MAXDEG; }

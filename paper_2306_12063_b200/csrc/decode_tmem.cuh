@@ -357,10 +357,21 @@ inline cudaError_t launch_tmem(const SpecArgs& a, cudaStream_t s) {
   auto kern = decode_tmem_kernel<S, A, ZS, ET>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
-  if (blocks <= 0) return cudaSuccess;
-  kern<<<(unsigned)blocks, threads, smem, s>>>(a);
-  return cudaGetLastError();
+  // the register count is only known after ptxas: shrink the CTA if this
+  // kernel cannot launch the planned one (the decode result does not depend
+  // on the CTA size)
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  if (threads > fa.maxThreadsPerBlock) {
+    SpecArgs b = a;
+    b.pairs = fa.maxThreadsPerBlock / z;
+    if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
+    if (b.tmem_cols > 0) return cudaErrorLaunchOutOfResources;   // TMEM plan is per CTA shape
+    return launch_layered_fixed(kern, b, z, RS, s);
+  }
+  return launch_layered_fixed(kern, a, z, RS, s);
 }
+
 
 }  // namespace qcb

@@ -4,17 +4,27 @@
 // i.e. the paper's Eqs. 12-15 on MSB-first packed blocks:
 //   S_i     = XOR_j P_{e_ij} u_j          (P_e = gather (r + e) mod Z: rotate left)
 //   v_0     = rot_fwd(XOR_i S_i, hb_y)    (cyclic_shift_packed, encoder.py:72-90)
-//   v_1     = S_0 ^ P_{hb_0} v_0
+//   v_1     = S_0 ^ P_{hb_0} v_0          (hb_0 < 0 acts as (hb_0 mod Z), encoder.py:93-100)
 //   v_{i+1} = v_i ^ S_i ^ [hb_i >= 0] P_{hb_i} v_0
-// A Z-bit block is held right-aligned in an unsigned __int128 (bit 0 of the
-// block = most significant of the Z bits), so both rotations are two shifts
-// and an OR.  The reference's word_bits choice (8/16/32) only changes how the
-// same bits are grouped; the encoded bytes are identical.
+// The reference's word_bits choice (8/16/32) only changes how the same bits
+// are grouped; the encoded bytes are identical for every choice.
 //
-// Data path (HBM-bound): one CTA stages 128 codewords of info bytes into
-// shared memory with 16-byte coalesced loads, one thread encodes one
-// codeword from shared memory, and the CTA writes the 128 codewords back
-// with 16-byte coalesced stores.  Grid-stride over CTA tiles.
+// Data path (HBM-bound: K/8 bytes in + N/8 bytes out per codeword): a CTA
+// stages 128 codewords of info bytes into shared memory with coalesced
+// 4-byte loads, one thread encodes one codeword, the CTA writes the 128
+// codewords back with coalesced 4-byte stores; grid-stride over tiles.
+//
+// Three encoders, chosen per code:
+//  * encode_z96_kernel<S>    native WiMAX Z = 96 codes (structure's own
+//    SHIFT0): a block is three big-endian 32-bit words, every circulant
+//    rotation has a compile-time shift and costs three funnel shifts; the
+//    tier structure is unrolled from structures_gen.cuh, all S_i in registers;
+//  * encode_struct_kernel<S> other codes of a known structure: same unrolled
+//    structure, runtime shifts, blocks in unsigned __int128 registers;
+//  * encode_generic_kernel   any other shift table: runtime loops, the S_i
+//    accumulate in the shared-memory output row (no local-memory arrays).
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,116 +33,406 @@ namespace qcb {
 constexpr int kEncThreads = 128;
 typedef unsigned __int128 u128;
 
+__host__ __device__ constexpr int enc_stride(int bytes) { return ((bytes + 3) & ~3) | 4; }
+
+// ---- staging ----------------------------------------------------------------------
+__device__ __forceinline__ void stage_in(const uint8_t* gin, uint8_t* sin, int ncw, int kbytes, int stride) {
+  const int total = ncw * kbytes;
+  if ((kbytes & 3) == 0 && (reinterpret_cast<uintptr_t>(gin) & 3) == 0) {
+    const uint32_t* g4 = reinterpret_cast<const uint32_t*>(gin);
+    const int kw = kbytes >> 2;
+    for (int i = threadIdx.x; i < total >> 2; i += blockDim.x) {
+      const int q = i / kw, o = i - q * kw;
+      *reinterpret_cast<uint32_t*>(sin + q * stride + 4 * o) = __ldcs(g4 + i);
+    }
+  } else {
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int q = i / kbytes, o = i - q * kbytes;
+      sin[q * stride + o] = gin[i];
+    }
+  }
+}
+
+__device__ __forceinline__ void stage_out(uint8_t* gout, const uint8_t* sout, int ncw, int nbytes, int stride) {
+  const int total = ncw * nbytes;
+  if ((nbytes & 3) == 0 && (reinterpret_cast<uintptr_t>(gout) & 3) == 0) {
+    uint32_t* g4 = reinterpret_cast<uint32_t*>(gout);
+    const int nw = nbytes >> 2;
+    for (int i = threadIdx.x; i < total >> 2; i += blockDim.x) {
+      const int q = i / nw, o = i - q * nw;
+      __stcs(g4 + i, *reinterpret_cast<const uint32_t*>(sout + q * stride + 4 * o));
+    }
+  } else {
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int q = i / nbytes, o = i - q * nbytes;
+      gout[i] = sout[q * stride + o];
+    }
+  }
+}
+
+// ---- compile-time structure queries -----------------------------------------------
+template <class S>
+constexpr int entry_at(int t, int j) {   // entry index of block (t, j); -1 = zero block
+  for (int e = S::START[t]; e < S::START[t + 1]; ++e)
+    if (S::COL[e] == j) return e;
+  return -1;
+}
+
+template <class S>
+constexpr int hb_y_shift() {             // the single interior h_b entry (find_y, encoder.py:39-46)
+  for (int t = 1; t < S::MB - 1; ++t)
+    if (entry_at<S>(t, S::KB) >= 0) return S::SHIFT0[entry_at<S>(t, S::KB)];
+  return 0;
+}
+
+// ---- Z = 96 with compile-time shifts: a block is 3 big-endian words ----------------
+struct B96 { uint32_t w[3]; };
+
+template <int E>
+__device__ __forceinline__ B96 rotl96(const B96& x) {   // out bit p = in bit (p + E) mod 96
+  constexpr int sw = E / 32, sb = E % 32;
+  B96 o;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t hi = x.w[(i + sw) % 3], lo = x.w[(i + sw + 1) % 3];
+    o.w[i] = sb == 0 ? hi : __funnelshift_l(lo, hi, sb);
+  }
+  return o;
+}
+__device__ __forceinline__ void xor_into(B96& a, const B96& b) {
+  a.w[0] ^= b.w[0]; a.w[1] ^= b.w[1]; a.w[2] ^= b.w[2];
+}
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+template <class S, int T, int J>
+__device__ __forceinline__ void acc96(B96& s, const B96 (&u)[S::KB]) {
+  constexpr int e = entry_at<S>(T, J);
+  if constexpr (e >= 0) xor_into(s, rotl96<S::SHIFT0[e]>(u[J]));
+}
+template <class S, int T, int... Js>
+__device__ __forceinline__ void row96(B96& s, const B96 (&u)[S::KB], std::integer_sequence<int, Js...>) {
+  s = B96{{0u, 0u, 0u}};
+  (acc96<S, T, Js>(s, u), ...);
+}
+template <class S, int... Ts>
+__device__ __forceinline__ void rows96(B96 (&s)[S::MB], const B96 (&u)[S::KB], std::integer_sequence<int, Ts...>) {
+  (row96<S, Ts>(s[Ts], u, std::make_integer_sequence<int, S::KB>{}), ...);
+}
+template <class S, int T>
+__device__ __forceinline__ void hb96(B96& v, const B96& v0) {   // v ^= P_{hb_T} v0 when hb_T >= 0
+  constexpr int e = entry_at<S>(T, S::KB);
+  if constexpr (e >= 0) xor_into(v, rotl96<S::SHIFT0[e]>(v0));
+}
+template <class S, int T>
+__device__ __forceinline__ void chain96(B96 (&v)[S::MB], const B96 (&s)[S::MB]) {   // encoder.py:193-197
+  if constexpr (T + 1 < S::MB) {
+    v[T + 1] = v[T];
+    xor_into(v[T + 1], s[T]);
+    hb96<S, T>(v[T + 1], v[0]);
+    chain96<S, T + 1>(v, s);
+  }
+}
+
+// Bulk-copy (TMA) pipeline: info tiles arrive by cp.async.bulk into a double
+// buffer completing on an mbarrier, codeword tiles leave by one bulk store
+// per tile.  While a CTA encodes tile i, tile i+1 (and i+2) is in flight in
+// and tile i-1 is draining out, so the kernel streams at HBM rate with only
+// two 128-thread CTAs per SM.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(dst), "r"(smem_u32(src)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <class S>
+struct Z96Tile {
+  static constexpr int KW = S::KB * 3, NW = S::NB * 3;          // 32-bit words per codeword
+  static constexpr int IN_BYTES = kEncThreads * KW * 4, OUT_BYTES = kEncThreads * NW * 4;
+  static constexpr size_t SMEM = 2 * (size_t)IN_BYTES + OUT_BYTES + 16;
+  static_assert(KW % 2 == 0 && NW % 4 == 0, "8-byte loads / 16-byte stores");
+};
+
+// One codeword: raw (byte-order) info words in, full codeword words out.
+template <class S>
+__device__ __forceinline__ void encode96_words(const uint32_t (&raw)[S::KB * 3], uint32_t (&o)[S::NB * 3]) {
+  B96 u[S::KB];
+#pragma unroll
+  for (int j = 0; j < S::KB; ++j)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) u[j].w[q] = bswap32(raw[3 * j + q]);
+  B96 s[S::MB];
+  rows96<S>(s, u, std::make_integer_sequence<int, S::MB>{});
+  B96 ssum = s[0];
+#pragma unroll
+  for (int i = 1; i < S::MB; ++i) xor_into(ssum, s[i]);
+  B96 v[S::MB];
+  v[0] = rotl96<(96 - hb_y_shift<S>()) % 96>(ssum);     // cyclic_shift_packed(ssum, hb_y)
+  v[1] = s[0];
+  hb96<S, 0>(v[1], v[0]);                                // encoder.py:192
+  chain96<S, 1>(v, s);                                   // encoder.py:193-197
+#pragma unroll
+  for (int k = 0; k < S::KB * 3; ++k) o[k] = raw[k];     // systematic bytes unchanged
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) o[3 * S::KB + 3 * i + q] = bswap32(v[i].w[q]);
+}
+
+// a.w must be a multiple of kEncThreads here (the host runs the tail through
+// encode_struct_kernel); a.info / a.cw 16-byte aligned.
+template <class S>
+__global__ void __launch_bounds__(kEncThreads, 2) encode_z96_kernel(const __grid_constant__ EncodeArgs a) {
+  using T = Z96Tile<S>;
+  static_assert(entry_at<S>(0, S::KB) >= 0, "h_b column must start with a non-zero block");
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint8_t* inbuf = sm;                                    // 2 x IN_BYTES, dense rows of KW words
+  uint8_t* outbuf = sm + 2 * T::IN_BYTES;                 // OUT_BYTES, dense rows of NW words
+  uint64_t* bar = reinterpret_cast<uint64_t*>(outbuf + T::OUT_BYTES);
+  const int64_t tiles = a.w / kEncThreads;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      const int64_t tl = blockIdx.x + (int64_t)b * gridDim.x;
+      if (tl < tiles) bulk_load(inbuf + b * T::IN_BYTES, a.info + tl * T::IN_BYTES, T::IN_BYTES, &bar[b]);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
+    uint32_t raw[T::KW], o[T::NW];
+    const uint2* in2 = reinterpret_cast<const uint2*>(inbuf + b * T::IN_BYTES + tid * T::KW * 4);
+#pragma unroll
+    for (int k = 0; k < T::KW / 2; ++k) {                 // LDS.64: odd 8-byte stride, no conflicts
+      const uint2 x = in2[k];
+      raw[2 * k] = x.x;
+      raw[2 * k + 1] = x.y;
+    }
+    encode96_words<S>(raw, o);
+    if (tid == 0) bulk_wait_read();                       // previous tile's store has left outbuf
+    __syncthreads();                                      // everyone is done with inbuf[b]
+    if (tid == 0) {
+      const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
+      if (nxt < tiles) {
+        fence_async_smem();
+        bulk_load(inbuf + b * T::IN_BYTES, a.info + nxt * T::IN_BYTES, T::IN_BYTES, &bar[b]);
+      }
+    }
+    uint4* out4 = reinterpret_cast<uint4*>(outbuf + tid * T::NW * 4);
+#pragma unroll
+    for (int k = 0; k < T::NW / 4; ++k) out4[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+    fence_async_smem();                                   // generic-proxy writes -> bulk store
+    __syncthreads();
+    if (tid == 0) bulk_store(a.cw + tile * T::OUT_BYTES, outbuf, T::OUT_BYTES);
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---- runtime shifts, blocks right-aligned in unsigned __int128 ----------------------
 __device__ __forceinline__ u128 rotl_z(u128 b, int e, int z, u128 mask) {
   if (e == 0) return b;
   return ((b << e) | (b >> (z - e))) & mask;
 }
-
 __device__ __forceinline__ u128 load_block(const uint8_t* p, int zb) {
   u128 v = 0;
   for (int i = 0; i < zb; ++i) v = (v << 8) | p[i];
   return v;
 }
-
 __device__ __forceinline__ void store_block(uint8_t* p, u128 v, int zb) {
   for (int i = zb - 1; i >= 0; --i) { p[i] = (uint8_t)v; v >>= 8; }
 }
+__device__ __forceinline__ u128 z_mask(int z) { return z == 128 ? ~u128(0) : ((u128(1) << z) - 1); }
 
-__global__ void __launch_bounds__(kEncThreads) encode_packed_kernel(const __grid_constant__ EncodeArgs a) {
+template <class S, int T, int J>
+__device__ __forceinline__ void acc_rt(u128& s, const u128& uj, const EncodeArgs& a, u128 mask) {
+  if constexpr (entry_at<S>(T, J) >= 0) s ^= rotl_z(uj, a.shifts[T * S::NB + J], a.z, mask);
+}
+template <class S, int J, int... Ts>
+__device__ __forceinline__ void col_rt(u128 (&s)[S::MB], const u128& uj, const EncodeArgs& a, u128 mask,
+                                       std::integer_sequence<int, Ts...>) {
+  (acc_rt<S, Ts, J>(s[Ts], uj, a, mask), ...);
+}
+template <class S, int... Js>
+__device__ __forceinline__ void cols_rt(u128 (&s)[S::MB], const uint8_t* u, int zb, const EncodeArgs& a,
+                                        u128 mask, std::integer_sequence<int, Js...>) {
+  (col_rt<S, Js>(s, load_block(u + Js * zb, zb), a, mask, std::make_integer_sequence<int, S::MB>{}), ...);
+}
+
+template <class S>
+__global__ void __launch_bounds__(kEncThreads) encode_struct_kernel(const __grid_constant__ EncodeArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int z = a.z, mb = a.mb, nb = a.nb, kb = nb - mb;
-  const int zb = z >> 3, kbytes = kb * zb, nbytes = nb * zb;
-  const int in_stride = ((kbytes + 3) & ~3) | 4;   // 4-byte aligned, odd word count (banks)
-  const int out_stride = ((nbytes + 3) & ~3) | 4;
+  const int z = a.z, zb = z >> 3, kbytes = S::KB * zb, nbytes = S::NB * zb;
+  const int in_stride = enc_stride(kbytes), out_stride = enc_stride(nbytes);
   uint8_t* sin = sm;
   uint8_t* sout = sm + kEncThreads * in_stride;
-  const u128 mask = (z == 128) ? ~u128(0) : ((u128(1) << z) - 1);
-
+  const u128 mask = z_mask(z);
   for (int64_t tile = blockIdx.x; tile * kEncThreads < a.w; tile += gridDim.x) {
     const int64_t cw0 = tile * kEncThreads;
     const int ncw = (int)(a.w - cw0 < kEncThreads ? a.w - cw0 : kEncThreads);
-    // ---- stage info bytes (coalesced 4-byte words when aligned) ----------
-    const uint8_t* gin = a.info + cw0 * kbytes;
-    const int total_in = ncw * kbytes;
-    if ((kbytes & 3) == 0 && (reinterpret_cast<uintptr_t>(gin) & 3) == 0) {
-      const uint32_t* g4 = reinterpret_cast<const uint32_t*>(gin);
-      const int kw = kbytes >> 2;
-      for (int i = threadIdx.x; i < total_in >> 2; i += blockDim.x) {
-        const int q = i / kw, o = i - q * kw;
-        *reinterpret_cast<uint32_t*>(sin + q * in_stride + 4 * o) = __ldcs(g4 + i);
-      }
-    } else {
-      for (int i = threadIdx.x; i < total_in; i += blockDim.x) {
-        const int q = i / kbytes, o = i - q * kbytes;
-        sin[q * in_stride + o] = gin[i];
-      }
-    }
+    stage_in(a.info + cw0 * kbytes, sin, ncw, kbytes, in_stride);
     __syncthreads();
-    // ---- encode one codeword per thread ------------------------------------
     if (threadIdx.x < ncw) {
       const uint8_t* u = sin + threadIdx.x * in_stride;
       uint8_t* out = sout + threadIdx.x * out_stride;
-      u128 s[12];
+      u128 s[S::MB];
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i) s[i] = 0;
+      cols_rt<S>(s, u, zb, a, mask, std::make_integer_sequence<int, S::KB>{});
       u128 ssum = 0;
-      for (int i = 0; i < mb; ++i) s[i] = 0;
-      for (int j = 0; j < kb; ++j) {
-        const u128 uj = load_block(u + j * zb, zb);
-        for (int i = 0; i < mb; ++i) {
-          const int e = a.shifts[i * nb + j];
-          if (e >= 0) s[i] ^= rotl_z(uj, e, z, mask);
-        }
-      }
-      for (int i = 0; i < mb; ++i) ssum ^= s[i];
-      // v0 = cyclic_shift_packed(ssum, hb_shift): forward rotation = rotl by (z - hb) mod z
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i) ssum ^= s[i];
       const u128 v0 = rotl_z(ssum, (z - a.hb_shift) % z, z, mask);
       store_block(out + kbytes, v0, zb);
-      if (mb >= 2) {
-        u128 v = s[0] ^ rotl_z(v0, a.shifts[kb], z, mask);   // v1 (encoder.py:192)
-        store_block(out + kbytes + zb, v, zb);
-        for (int i = 1; i < mb - 1; ++i) {                    // encoder.py:193-197
-          v ^= s[i];
-          const int hb = a.shifts[i * nb + kb];
-          if (hb >= 0) v ^= rotl_z(v0, hb, z, mask);
-          store_block(out + kbytes + (i + 1) * zb, v, zb);
-        }
+      u128 v = s[0] ^ rotl_z(v0, (a.shifts[S::KB] % z + z) % z, z, mask);
+      store_block(out + kbytes + zb, v, zb);
+#pragma unroll
+      for (int i = 1; i < S::MB - 1; ++i) {
+        v ^= s[i];
+        const int hb = a.shifts[i * S::NB + S::KB];
+        if (hb >= 0) v ^= rotl_z(v0, hb, z, mask);
+        store_block(out + kbytes + (i + 1) * zb, v, zb);
       }
       for (int b = 0; b < kbytes; ++b) out[b] = u[b];
     }
     __syncthreads();
-    // ---- write codewords back (coalesced) ----------------------------------
-    uint8_t* gout = a.cw + cw0 * nbytes;
-    const int total_out = ncw * nbytes;
-    if ((nbytes & 3) == 0 && (reinterpret_cast<uintptr_t>(gout) & 3) == 0) {
-      uint32_t* g4 = reinterpret_cast<uint32_t*>(gout);
-      const int nw = nbytes >> 2;
-      for (int i = threadIdx.x; i < total_out >> 2; i += blockDim.x) {
-        const int q = i / nw, o = i - q * nw;
-        __stcs(g4 + i, *reinterpret_cast<const uint32_t*>(sout + q * out_stride + 4 * o));
-      }
-    } else {
-      for (int i = threadIdx.x; i < total_out; i += blockDim.x) {
-        const int q = i / nbytes, o = i - q * nbytes;
-        gout[i] = sout[q * out_stride + o];
-      }
-    }
+    stage_out(a.cw + cw0 * nbytes, sout, ncw, nbytes, out_stride);
     __syncthreads();
   }
 }
 
-cudaError_t launch_encode_packed(const EncodeArgs& a, cudaStream_t s) {
-  if (a.w <= 0) return cudaSuccess;
-  const int zb = a.z >> 3, kb = a.nb - a.mb;
-  const int in_stride = ((kb * zb + 3) & ~3) | 4, out_stride = ((a.nb * zb + 3) & ~3) | 4;
-  const size_t smem = (size_t)kEncThreads * (in_stride + out_stride);
-  cudaError_t e = cudaFuncSetAttribute(encode_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
+__global__ void __launch_bounds__(kEncThreads) encode_generic_kernel(const __grid_constant__ EncodeArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int z = a.z, mb = a.mb, nb = a.nb, kb = nb - mb;
+  const int zb = z >> 3, kbytes = kb * zb, nbytes = nb * zb;
+  const int in_stride = enc_stride(kbytes), out_stride = enc_stride(nbytes);
+  uint8_t* sin = sm;
+  uint8_t* sout = sm + kEncThreads * in_stride;
+  const u128 mask = z_mask(z);
+  for (int64_t tile = blockIdx.x; tile * kEncThreads < a.w; tile += gridDim.x) {
+    const int64_t cw0 = tile * kEncThreads;
+    const int ncw = (int)(a.w - cw0 < kEncThreads ? a.w - cw0 : kEncThreads);
+    stage_in(a.info + cw0 * kbytes, sin, ncw, kbytes, in_stride);
+    __syncthreads();
+    if (threadIdx.x < ncw) {
+      const uint8_t* u = sin + threadIdx.x * in_stride;
+      uint8_t* out = sout + threadIdx.x * out_stride;
+      uint8_t* par = out + kbytes;                 // S_i accumulate in the output row
+      for (int i = 0; i < mb; ++i) store_block(par + i * zb, 0, zb);
+      for (int j = 0; j < kb; ++j) {
+        const u128 uj = load_block(u + j * zb, zb);
+        for (int i = 0; i < mb; ++i) {
+          const int e = a.shifts[i * nb + j];
+          if (e >= 0) store_block(par + i * zb, load_block(par + i * zb, zb) ^ rotl_z(uj, e, z, mask), zb);
+        }
+      }
+      u128 ssum = 0;
+      for (int i = 0; i < mb; ++i) ssum ^= load_block(par + i * zb, zb);
+      const u128 v0 = rotl_z(ssum, (z - a.hb_shift) % z, z, mask);
+      const u128 s0 = load_block(par, zb);
+      store_block(par, v0, zb);
+      u128 v = s0 ^ rotl_z(v0, (a.shifts[kb] % z + z) % z, z, mask);
+      for (int i = 1; i < mb - 1; ++i) {
+        const u128 si = load_block(par + i * zb, zb);
+        store_block(par + i * zb, v, zb);
+        v ^= si;
+        const int hb = a.shifts[i * nb + kb];
+        if (hb >= 0) v ^= rotl_z(v0, hb, z, mask);
+      }
+      store_block(par + (mb - 1) * zb, v, zb);
+      for (int b = 0; b < kbytes; ++b) out[b] = u[b];
+    }
+    __syncthreads();
+    stage_out(a.cw + cw0 * nbytes, sout, ncw, nbytes, out_stride);
+    __syncthreads();
+  }
+}
+
+static int64_t enc_grid(const void* kern, size_t smem, int64_t tiles, cudaError_t* err) {
+  int dev = 0, sms = 148, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tiles = (a.w + kEncThreads - 1) / kEncThreads;
-  const int64_t grid = tiles < (int64_t)sms * 8 ? tiles : (int64_t)sms * 8;
-  encode_packed_kernel<<<(unsigned)grid, kEncThreads, smem, s>>>(a);
+  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
+  if (*err != cudaSuccess) return 0;
+  if (per_sm < 1) { *err = cudaErrorLaunchOutOfResources; return 0; }
+  const int64_t cap = (int64_t)sms * per_sm;
+  return tiles < cap ? tiles : cap;
+}
+
+template <class K>
+static cudaError_t launch_enc(K kern, const EncodeArgs& a, cudaStream_t s) {
+  const int zb = a.z >> 3, kbytes = (a.nb - a.mb) * zb, nbytes = a.nb * zb;
+  const size_t smem = (size_t)kEncThreads * (enc_stride(kbytes) + enc_stride(nbytes));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = enc_grid((const void*)kern, smem, (a.w + kEncThreads - 1) / kEncThreads, &e);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, kEncThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// native Z = 96: full tiles through the bulk-copy pipeline, the ragged tail
+// (and misaligned buffers) through the staged kernel.
+template <class S>
+static cudaError_t launch_z96(const EncodeArgs& a, cudaStream_t s) {
+  using T = Z96Tile<S>;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.info) | reinterpret_cast<uintptr_t>(a.cw)) & 15) == 0;
+  const int64_t full = aligned ? a.w / kEncThreads * kEncThreads : 0;
+  if (full > 0) {
+    cudaError_t e = cudaFuncSetAttribute(encode_z96_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)T::SMEM);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = enc_grid((const void*)encode_z96_kernel<S>, T::SMEM, full / kEncThreads, &e);
+    if (e != cudaSuccess) return e;
+    EncodeArgs b = a;
+    b.w = full;
+    encode_z96_kernel<S><<<(unsigned)grid, kEncThreads, T::SMEM, s>>>(b);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (full == a.w) return cudaSuccess;
+  EncodeArgs r = a;
+  r.info = a.info + full * (T::KW * 4);
+  r.cw = a.cw + full * (T::NW * 4);
+  r.w = a.w - full;
+  return launch_enc(encode_struct_kernel<S>, r, s);
+}
+
+cudaError_t launch_encode_packed(const EncodeArgs& a, int structure_id, cudaStream_t s) {
+  if (a.w <= 0) return cudaSuccess;
+  if (a.mb < 2) return cudaErrorInvalidValue;
+#define QCB_ENC(STRUCT)                                                         \
+  if (structure_id == STRUCT::ID && STRUCT::NB == a.nb && STRUCT::MB == a.mb) { \
+    if constexpr (STRUCT::Z0 == 96)                                             \
+      if (a.native && a.z == 96) return launch_z96<STRUCT>(a, s);               \
+    return launch_enc(encode_struct_kernel<STRUCT>, a, s);                      \
+  }
+  QCB_FOR_EACH_STRUCTURE(QCB_ENC)
+#undef QCB_ENC
+  return launch_enc(encode_generic_kernel, a, s);
 }
 
 }  // namespace qcb

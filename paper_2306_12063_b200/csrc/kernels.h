@@ -37,6 +37,7 @@ struct SpecArgs {
   int32_t n, z, max_iters, early_term, hard_packed;
   int32_t pairs;   // codewords per CTA
   int32_t tmem_cols;  // TMEM columns per CTA (TMEM-resident message kernel), 0 = register kernel
+  int32_t native;     // 1: z == S::Z0 and shifts == S::SHIFT0 (compile-time shift kernel)
   uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
   int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
@@ -47,6 +48,8 @@ cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStrea
 int spec_row_stride_bytes(int elem);   // bytes per c-row of the shared-memory layout
 int spec_cw_per_cta(int z, int64_t w);
 void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols);
+// true when (z, tier-major shifts) equal the structure's native Z0 / SHIFT0 tables
+bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne);
 
 // Packed direct encoder (encoder.py:166-199), byte-aligned Z.
 struct EncodeArgs {
@@ -54,8 +57,10 @@ struct EncodeArgs {
   uint8_t* cw;           // W x N/8
   int64_t w;
   int32_t mb, nb, z, hb_shift;
+  int32_t native;           // 1: shifts are the structure's native SHIFT0 at Z0
   int32_t shifts[12 * 24];  // mb x nb, -1 = zero block
 };
-cudaError_t launch_encode_packed(const EncodeArgs& a, cudaStream_t s);
+// structure_id: index into kStructureMasks, -1 = generic
+cudaError_t launch_encode_packed(const EncodeArgs& a, int structure_id, cudaStream_t s);
 
 }  // namespace qcb

@@ -7,11 +7,11 @@ namespace qcb {
 template <class S, class A>
 static cudaError_t launch_arith(const SpecArgs& a, cudaStream_t s) {
   if (a.tmem_cols > 0) {
-    if (a.z == S::Z0)
+    if (a.native)
       return a.early_term ? launch_tmem<S, A, S::Z0, true>(a, s) : launch_tmem<S, A, S::Z0, false>(a, s);
     return a.early_term ? launch_tmem<S, A, 0, true>(a, s) : launch_tmem<S, A, 0, false>(a, s);
   }
-  if (a.z == S::Z0)
+  if (a.native)
     return a.early_term ? launch_layered<S, A, S::Z0, true>(a, s) : launch_layered<S, A, S::Z0, false>(a, s);
   return a.early_term ? launch_layered<S, A, 0, true>(a, s) : launch_layered<S, A, 0, false>(a, s);
 }

@@ -145,6 +145,35 @@ def test_generic_kernel_on_nonstandard_codes():
                 assert _post_equal(post, op)
 
 
+def test_standard_structure_with_foreign_shifts():
+    """A standard zero-block pattern at its native Z but with other shift values
+    must not take the compile-time-shift kernels (decoder and encoder)."""
+    rng = np.random.default_rng(17)
+    for std, n, rate in (("wimax", 2304, "1/2"), ("wimax", 2304, "3/4A"), ("wifi", 1944, "5/6"),
+                         ("wifi", 648, "1/2")):
+        base = P.get_model_matrix(std, n, rate)
+        ent = base.entries.copy()
+        nz = ent >= 0
+        ent[nz] = rng.integers(0, base.z, size=int(nz.sum()))
+        ent[:, base.kb:] = base.entries[:, base.kb:]          # keep the dual-diagonal part
+        mm = P.ModelMatrix(base.standard, base.rate, base.z, base.nb, base.kb, ent)
+        assert P.code_handle(mm).specialised
+        h = P.expand(mm)
+        for fixed in (False, True):
+            llr, _, _ = noisy_llrs(mm, 7, 3.0, seed=int(rng.integers(1 << 30)), fixed=fixed)
+            cfg = P.DecoderConfig(max_iterations=5, early_termination=False,
+                                  arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
+            hard, it, conv, post = _gpu(mm, llr, cfg)
+            oh, oi, oc, op = O.decode_batch(h, llr, 5, False, want_post=True)
+            assert np.array_equal(hard, oh) and np.array_equal(conv, oc), (std, n, rate, fixed)
+            assert _post_equal(post, op), (std, n, rate, fixed)
+        if mm.z % 8 == 0:
+            info = rng.integers(0, 256, size=(300, mm.k // 8), dtype=np.uint8)
+            plan = P.make_plan(mm, P.EncoderVariant.Packed)
+            dev = P.encode_packed(plan, torch.from_numpy(info).cuda()).cpu().numpy()
+            assert np.array_equal(dev, O.encode_packed(mm, info)), (std, n, rate)
+
+
 def test_known_answers(golden_dir):
     kat = np.load(golden_dir / "kat.npz")
     toy = P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 1, 3, 2, np.array([[0, 0, 0]]))
@@ -279,6 +308,22 @@ def test_packed_encoder_all_octet_codes_vs_oracle_and_array():
         got = P.encode_packed(P.make_plan(mm, P.EncoderVariant.Packed), ib)
         assert np.array_equal(got, O.encode_packed(mm, ib)), (n, rate)
         assert np.array_equal(got, P.pack_bits(P.encode_array(P.make_plan(mm), info))), (n, rate)
+
+
+@pytest.mark.parametrize("rate", ["1/2", "2/3A", "2/3B", "3/4A", "3/4B", "5/6"])
+def test_packed_encoder_native_z96_tiles_tail_and_misaligned(rate):
+    """Native Z=96 codes take the bulk-copy pipeline for whole 128-codeword
+    tiles and the staged kernel for the ragged tail / misaligned buffers."""
+    mm = P.get_model_matrix("wimax", 2304, rate)
+    plan = P.make_plan(mm, P.EncoderVariant.Packed)
+    rng = np.random.default_rng(hash(rate) % 1000)
+    info = rng.integers(0, 256, size=(128 * 700 + 77, mm.k // 8), dtype=np.uint8)
+    ref = O.encode_packed(mm, info)
+    dev = torch.from_numpy(info).cuda()
+    assert np.array_equal(P.encode_packed(plan, dev).cpu().numpy(), ref)
+    sub = dev[1:257]                                    # 8-byte-misaligned view
+    assert np.array_equal(P.encode_packed(plan, sub).cpu().numpy(), ref[1:257])
+    assert np.array_equal(P.encode_packed(plan, dev[:128 * 3]).cpu().numpy(), ref[:128 * 3])
 
 
 def test_encode_then_decode_round_trip_c5_scale():
