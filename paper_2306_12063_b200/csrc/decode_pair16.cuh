@@ -1,0 +1,332 @@
+// decode_pair16.cuh -- int16 layered min-sum, two codewords per thread in
+// 16x2 SIMD lanes (sm_100a).
+//
+// Reference: /root/reference/pkg/src/qcldpc/_kernels.py:103-186 (int16 with
+// two's-complement wrap after every op).  The reference's int16 values are
+// 16 bits wide, so one 32-bit register carries the same row of TWO
+// codewords: the low lane belongs to codeword 2g, the high lane to 2g+1.
+// Every per-edge operation is a lane-wise 16-bit operation with the
+// reference's wrap (VIADD.16x2 adds wrap per lane; VIMNMX.S16x2 compares in
+// signed int16 order, so abs(-32768) = -32768 sorts lowest exactly as in the
+// reference).  One instruction therefore advances two codewords, and one
+// 32-bit shared-memory access moves both codewords' posterior.
+//
+// Messages are kept NEGATED (nm = -L_mn) so that zz = post - L_old is a
+// single lane-wise add.  Lane-wise negation / sign application use
+// -x = ~x + 1 with ~x = x * (-1) + (-1) on the FMA pipe (a 32-bit IMAD
+// cannot carry across lanes for this operand), so the row update splits
+// about evenly between the half-rate ALU and FMA-heavy pipes:
+//   pass 1  d = p + nm                                   (VIADD.16x2)
+//           a = max(d, ~d + 0x10001) = |d| (wrapping)    (IMAD, VIADD, VIMNMX)
+//   minima  ex_k = min_{j != k} a_j (prefix / suffix)    (VIMNMX)
+//   pass 2  m    = lane sign mask of d ^ parity          (LOP3, PRMT)
+//           L    = (ex ^ m) + (m & 0x10001)  = +-ex      (LOP3, LOP3, VIADD)
+//           post = d + L, nm = ~(ex ^ m) + (0x10001 - (m & 0x10001))
+// Shared memory layout, addressing and tier schedule are the float32
+// kernel's (4-byte cells, decode_layered.cuh).
+#pragma once
+#include "decode_layered.cuh"
+
+namespace qcb {
+
+__device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
+  uint32_t d; asm("add.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
+  uint32_t d; asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) {
+  uint32_t d; asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+// lane sign masks: 0xFFFF in a lane whose bit 15 is set
+__device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
+  uint32_t d; asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x)); return d;
+}
+
+struct RtK2 {             // runtime constants (kernel parameters): keep IMAD operands out of ptxas' reach
+  uint32_t one, neg1, lane1;   // 1, 0xFFFFFFFF, 0x00010001
+};
+
+struct ArithI16x2 {
+  using Val = uint32_t;
+  static constexpr int kElem = 4;        // one cell = the two codewords' int16 posteriors
+
+  __device__ static Val lds(uint32_t a) { uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
+  __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+
+  template <int D>
+  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* nm, const RtK2& K) {
+    static_assert(D >= 2, "row degree >= 2");
+    uint32_t d[D], a[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      d[k] = vadd2(p[k], nm[k]);                                   // zz = post - L_old
+      a[k] = vmax2(d[k], vadd2(imad(d[k], K.neg1, K.neg1), K.lane1));   // |zz| (wrapping)
+    }
+    uint32_t sx = 0;                                               // lane parities in bits 15 / 31
+#pragma unroll
+    for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
+    if (D & 1) sx ^= d[D - 1];
+    uint32_t pre[D], suf[D], ex[D];
+    pre[1] = a[0];
+#pragma unroll
+    for (int k = 2; k < D; ++k) pre[k] = vmin2(pre[k - 1], a[k - 1]);
+    suf[D - 2] = a[D - 1];
+#pragma unroll
+    for (int k = D - 3; k >= 0; --k) suf[k] = vmin2(suf[k + 1], a[k + 1]);
+    ex[0] = suf[0];
+    ex[D - 1] = pre[D - 1];
+#pragma unroll
+    for (int k = 1; k < D - 1; ++k) ex[k] = vmin2(pre[k], suf[k]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
+      const uint32_t t1 = ex[k] ^ m, t2 = m & 0x00010001u;
+      const uint32_t l = vadd2(t1, t2);                            // +-ex, wrapping
+      o[k] = vadd2(d[k], l);                                       // post = zz + L_new
+      nm[k] = vadd2(imad(t1, K.neg1, K.neg1), imad(t2, K.neg1, K.lane1));   // -L_new
+    }
+  }
+};
+
+template <class S, int ZS>
+struct Layered2 {
+  using A = ArithI16x2;
+
+  // keep: lanes of converged codewords (early termination) keep their posteriors
+  template <int T, bool ET>
+  __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK2& K, int r, uint32_t b0, uint32_t b1,
+                                              uint32_t (&nm)[S::NE], uint32_t keep) {
+    constexpr int D = S::DEG[T];
+    constexpr int E0 = S::START[T];
+    uint32_t addr[D], p[D], o[D];
+    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+#pragma unroll
+    for (int k = 0; k < D; ++k) p[k] = A::lds(addr[k]);
+    A::template row<D>(p, o, nm + E0, K);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      uint32_t v = o[k];
+      if constexpr (ET) v = (v & ~keep) | (p[k] & keep);
+      A::sts(addr[k], v);
+    }
+  }
+
+  template <int T>
+  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+    constexpr int D = S::DEG[T];
+    constexpr int E0 = S::START[T];
+    uint32_t addr[D];
+    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    uint32_t par = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint32_t v = A::lds(addr[k]);
+      const int lo = sext16((int)v), hi = (int)v >> 16;           // hard = post <= 0 per lane
+      par ^= (lo <= 0 ? 1u : 0u) | (hi <= 0 ? 2u : 0u);
+    }
+    return par;
+  }
+
+  template <bool ET, int... Ts>
+  __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK2& K, int r, uint32_t b0, uint32_t b1,
+                                               uint32_t (&nm)[S::NE], bool work, uint32_t keep,
+                                               std::integer_sequence<int, Ts...>) {
+    if constexpr (ET) {
+      ((work ? tier<Ts, true>(a, K, r, b0, b1, nm, keep) : void(), __syncthreads()), ...);
+    } else {
+      (void)work; (void)keep;
+      ((tier<Ts, false>(a, K, r, b0, b1, nm, 0u), __syncthreads()), ...);
+    }
+  }
+
+  template <int... Ts>
+  __device__ __forceinline__ static uint32_t parity_all(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                        std::integer_sequence<int, Ts...>) {
+    return (parity<Ts>(a, r, b0, b1) | ...);
+  }
+};
+
+#ifndef QCB_P16_SLACK
+#define QCB_P16_SLACK 52
+#endif
+template <class S, int ZS>
+constexpr int p16_reg_cap() {
+  const int want = S::NE + QCB_P16_SLACK;
+  const int z = ZS > 0 ? ZS : 96;
+  const int threads = (cw_per_cta_large(z) * z + 31) / 32 * 32;
+  int ctas = 65536 / (threads * ((want + 7) / 8 * 8));
+  if (ctas < 1) ctas = 1;
+  int cap = 65536 / (threads * ctas) / 8 * 8;          // same CTA count, every spare register
+  if (cap < want) cap = (want + 7) / 8 * 8;
+  return cap > 255 ? 255 : cap;
+}
+
+// a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
+template <class S, int ZS, bool ET>
+__global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS>()))
+    decode_pair16_kernel(const __grid_constant__ SpecArgs a) {
+  using L = Layered2<S, ZS>;
+  constexpr int RS = row_stride_bytes<ArithI16x2>();
+  constexpr int MAXC = 2 * kLayMaxCw;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
+  __shared__ int s_active;
+
+  const RtK2 K{a.k_one, a.k_neg1, a.k_lane1};
+  const int Z = ZS > 0 ? ZS : a.z;
+  const int N = S::NB * Z;
+  const int G = a.pairs;
+  const int tid = threadIdx.x;
+  const int g = tid / Z, r = tid - g * Z;
+  const int64_t cw0 = (int64_t)blockIdx.x * (2 * G);
+  const int ncw = (int)(a.w - cw0 < (int64_t)(2 * G) ? a.w - cw0 : (int64_t)(2 * G));
+  const int npairs = (ncw + 1) >> 1;
+  const bool act = g < npairs;
+  const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const int gs = g < G ? g : G, rs = g < G ? r : (tid - G * Z) % Z;
+  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
+  asm volatile("mov.b32 %0, %0;" : "+r"(b0));
+  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+
+  // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
+  {
+    const int nthr = blockDim.x;
+    const short* llr = reinterpret_cast<const short*>(a.llr);
+    const bool al4 = ((reinterpret_cast<uintptr_t>(llr) | (uintptr_t)(N * 2)) & 3) == 0;
+    for (int q = 0; q < npairs; ++q) {
+      const uint32_t cb = sbase + (uint32_t)q * cws;
+      const short* sa = llr + (cw0 + 2 * q) * N;
+      const bool hasb = 2 * q + 1 < ncw;
+      const short* sb = hasb ? sa + N : sa;
+      if (al4) {
+        const uint32_t* ua = reinterpret_cast<const uint32_t*>(sa);
+        const uint32_t* ub = reinterpret_cast<const uint32_t*>(sb);
+        for (int i = tid; i < (N >> 1); i += nthr) {
+          const int n = 2 * i;
+          const int j = n / Z, c = n - j * Z;
+          const uint32_t x = __ldcs(ua + i), y = hasb ? __ldcs(ub + i) : 0u;
+          ArithI16x2::sts(cb + c * RS + j * 4, __byte_perm(x, y, 0x5410));
+          const int c1 = c + 1 == Z ? 0 : c + 1, j1 = c + 1 == Z ? j + 1 : j;
+          ArithI16x2::sts(cb + c1 * RS + j1 * 4, __byte_perm(x, y, 0x7632));
+        }
+      } else {
+        for (int n = tid; n < N; n += nthr) {
+          const int j = n / Z, c = n - j * Z;
+          const uint32_t x = (uint16_t)__ldcs(sa + n), y = hasb ? (uint16_t)__ldcs(sb + n) : 0u;
+          ArithI16x2::sts(cb + c * RS + j * 4, x | (y << 16));
+        }
+      }
+    }
+    for (int q = tid; q < MAXC + 2; q += blockDim.x) {
+      s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
+    }
+  }
+  __syncthreads();
+
+  uint32_t nm[S::NE];
+#pragma unroll
+  for (int e = 0; e < S::NE; ++e) nm[e] = 0u;
+
+  const auto tiers = std::make_integer_sequence<int, S::MB>{};
+  for (int k = 0; k < a.max_iters; ++k) {
+    bool work = act;
+    uint32_t keep = 0;
+    if constexpr (ET) {
+      const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
+      work = act && !(da && db);
+      keep = (da ? 0x0000FFFFu : 0u) | (db ? 0xFFFF0000u : 0u);
+    }
+    L::template sweep<ET>(a, K, rs, b0, b1, nm, work, keep, tiers);
+    const bool last = (k + 1 == a.max_iters);
+    if (ET || last) {                           // syndrome (_kernels.py:85-96)
+      if (tid < MAXC) s_fail[tid] = 0;
+      __syncthreads();
+      if (work) {
+        const uint32_t par = L::parity_all(a, rs, b0, b1, tiers);
+        if (par & 1u) s_fail[2 * g] = 1;
+        if (par & 2u) s_fail[2 * g + 1] = 1;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_active = 0;
+    __syncthreads();
+    if (tid < ncw && !s_done[tid]) {
+      s_iters[tid] = k + 1;
+      if (ET && !s_fail[tid]) s_done[tid] = 1;
+      else s_active = 1;
+    }
+    __syncthreads();
+    if (!s_active) break;
+  }
+
+  // ---- outputs ---------------------------------------------------------------
+  if (tid < ncw) {
+    a.iters[cw0 + tid] = s_iters[tid];
+    a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
+  }
+  const int nthr = blockDim.x;
+  auto lane_val = [&](int q, int n) -> int {     // int16 posterior of codeword q (of this CTA), bit n
+    const int j = n / Z, c = n - j * Z;
+    const uint32_t v = ArithI16x2::lds(sbase + (uint32_t)(q >> 1) * cws + c * RS + j * 4);
+    return (q & 1) ? ((int)v >> 16) : sext16((int)v);
+  };
+  if (a.hard_packed) {
+    const int nbytes = (N + 7) >> 3;
+    uint8_t* hp = reinterpret_cast<uint8_t*>(a.hard) + cw0 * nbytes;
+    for (int i = tid; i < ncw * nbytes; i += nthr) {
+      const int q = i / nbytes, b = i - q * nbytes;
+      uint32_t byte = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int n = b * 8 + u;
+        byte = (byte << 1) | ((n < N && lane_val(q, n) <= 0) ? 1u : 0u);
+      }
+      hp[i] = (uint8_t)byte;
+    }
+  } else {
+    uint8_t* h = reinterpret_cast<uint8_t*>(a.hard) + cw0 * N;
+    for (int q = 0; q < ncw; ++q) {
+      for (int n4 = tid * 4; n4 < N; n4 += nthr * 4) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (n4 + u < N && lane_val(q, n4 + u) <= 0) word |= 1u << (8 * u);
+        uint8_t* dst = h + (int64_t)q * N + n4;
+        if (n4 + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) *reinterpret_cast<uint32_t*>(dst) = word;
+        else for (int u = 0; n4 + u < N; ++u) dst[u] = (uint8_t)(word >> (8 * u));
+      }
+    }
+  }
+  if (a.post) {
+    int16_t* po = reinterpret_cast<int16_t*>(a.post);
+    for (int q = 0; q < ncw; ++q)
+      for (int n = tid; n < N; n += nthr) po[(cw0 + q) * N + n] = (int16_t)lane_val(q, n);
+  }
+}
+
+template <class S, int ZS, bool ET>
+inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
+  constexpr int RS = row_stride_bytes<ArithI16x2>();
+  const int z = ZS > 0 ? ZS : a.z;
+  auto kern = decode_pair16_kernel<S, ZS, ET>;
+  SpecArgs b = a;
+  const int threads = (b.pairs * z + 31) / 32 * 32;
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  if (threads > fa.maxThreadsPerBlock) b.pairs = fa.maxThreadsPerBlock / z;
+  if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
+  const int thr = (b.pairs * z + 31) / 32 * 32;
+  const size_t smem = (size_t)(b.pairs + 1) * ((z * RS + 15) & ~15);   // + scratch slot
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t per = 2 * (int64_t)b.pairs;
+  const int64_t blocks = (a.w + per - 1) / per;
+  if (blocks <= 0) return cudaSuccess;
+  kern<<<(unsigned)blocks, thr, smem, s>>>(b);
+  return cudaGetLastError();
+}
+
+}  // namespace qcb

@@ -2,6 +2,7 @@
 // The kernel template lives in decode_layered.cuh; its 18 structures x
 // {float32, int16} x {native Z, runtime Z} x {early termination on, off}
 // instantiations are split over spec_part{0..5}.cu so they compile in parallel.
+#include "decode_pair16.cuh"
 #include "decode_tmem.cuh"
 
 namespace qcb {
@@ -45,8 +46,19 @@ bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne) {
   return native;
 }
 
-void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols) {
+void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
+               int32_t* pair16) {
   int ne = 0, maxdeg = 0;
+  *pair16 = 0;
+  if (elem == 2) {                          // int16: two codewords per thread in 16x2 lanes
+    const char* p = getenv("QCB_I16_PAIR");
+    if (!(p && p[0] == '0')) {
+      *pair16 = 1;
+      *cw_per_cta = layered_cw_per_cta(z, (w + 1) / 2);   // codeword pairs per CTA
+      *tmem_cols = 0;
+      return;
+    }
+  }
 #define QCB_NE(STRUCT) if (structure_id == STRUCT::ID) { ne = STRUCT::NE; maxdeg = STRUCT::MAXDEG; }
   QCB_FOR_EACH_STRUCTURE(QCB_NE)
 #undef QCB_NE

@@ -39,6 +39,8 @@ struct SpecArgs {
   int32_t tmem_cols;  // TMEM columns per CTA (TMEM-resident message kernel), 0 = register kernel
   int32_t native;     // 1: z == S::Z0 and shifts == S::SHIFT0 (compile-time shift kernel)
   uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
+  uint32_t k_lane1;   // 0x00010001 (16x2 lane constant)
+  int32_t pair16;     // int16 only: 1 = two codewords per thread in 16x2 lanes (pairs = codeword pairs per CTA)
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
   int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
 };
@@ -47,7 +49,8 @@ struct SpecArgs {
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
 int spec_row_stride_bytes(int elem);   // bytes per c-row of the shared-memory layout
 int spec_cw_per_cta(int z, int64_t w);
-void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols);
+void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
+               int32_t* pair16);
 // true when (z, tier-major shifts) equal the structure's native Z0 / SHIFT0 tables
 bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne);
 

@@ -1,11 +1,19 @@
 // spec_part2.cu -- instantiations of the layered decoder for the
 // structures with ID % 6 == 2 (see decode_spec.cu / decode_layered.cuh).
+#include "decode_pair16.cuh"
 #include "decode_tmem.cuh"
 
 namespace qcb {
 
 template <class S, class A>
 static cudaError_t launch_arith(const SpecArgs& a, cudaStream_t s) {
+  if constexpr (A::kElem == 2) {
+    if (a.pair16) {
+      if (a.native)
+        return a.early_term ? launch_pair16<S, S::Z0, true>(a, s) : launch_pair16<S, S::Z0, false>(a, s);
+      return a.early_term ? launch_pair16<S, 0, true>(a, s) : launch_pair16<S, 0, false>(a, s);
+    }
+  }
   if (a.tmem_cols > 0) {
     if (a.native)
       return a.early_term ? launch_tmem<S, A, S::Z0, true>(a, s) : launch_tmem<S, A, S::Z0, false>(a, s);
