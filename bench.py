@@ -338,6 +338,10 @@ def run_ours(args, wl):
     peaks, peak_kind = measured_peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    # the int16 kernel carries two codewords per 32-bit lane (16x2 SIMD):
+    # its peak counts 2x so the fraction stays <= 1
+    simd = 2 if (wl.fixed and os.environ.get("QCB_I16_PAIR", "1") != "0") else 1
+    alu_peak *= simd
     kavg = statistics.mean(kernel_ms) * 1e-3
     achieved = edge_updates(wl) * OPS_PER_EDGE_UPDATE / kavg / 1e12
     traffic, traffic_src = ncu_traffic(wl.key)
@@ -374,6 +378,7 @@ def run_ours(args, wl):
                          "note": f"{OPS_PER_EDGE_UPDATE} lane-ops per edge-update x {edge_updates(wl)} "
                                  f"edge-updates per launch / avg launch {kavg * 1e3:.3f} ms; peak = {sms} SMs x 128 "
                                  f"lanes x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz ({peak_kind} sm_max_mhz)"
+                                 + (" x 2 (int16 16x2 SIMD: two codewords per lane-op)" if simd == 2 else "")
                                  + (f"; traffic from {traffic_src}" if traffic_src else ""),
                          "hbm": {"achieved": round(hbm_ach, 1), "peak": peaks.get("hbm_gbs"),
                                  "unit": "GB/s", "frac": round(hbm_ach / peaks.get("hbm_gbs", 6650.0), 4)}},

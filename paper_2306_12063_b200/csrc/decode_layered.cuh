@@ -363,44 +363,97 @@ struct Layered {
 #ifndef QCB_REG_SLACK
 #define QCB_REG_SLACK 52
 #endif
-// codewords per CTA for a large batch: whole warps, small CTAs (one barrier
-// per tier).  The host uses the same rule (layered_cw_per_cta) and only
-// shrinks G further for small batches.
-constexpr int cw_per_cta_large(int z) {
+// CTA shape.  A CTA holds p codewords (p*Z threads, padded to whole warps).
+// Measured on B200 (tools/exp/ctasweep.py, 16384 f32 / 65536 int16
+// codewords, 10 iterations), coded Gbit/s for p = 1 / 2 / 3 / 4:
+//   f32  Wi-Fi 648 R1/2   38.0 / 39.5 / 39.4 / 38.5
+//   f32  Wi-Fi 1296 R1/2  46.6 / 44.8 / 39.4 / 27.9
+//   f32  Wi-Fi 1944 R1/2  47.8 / 41.4 / 32.3 / 34.0
+//   f32  WiMAX 2304 R1/2  71.9 / 60.9 / 40.7 / 47.3
+//   i16  Wi-Fi 1296 R1/2  58.8 / 57.0 / 47.1 / 34.7
+//   i16  WiMAX 2304 R3/4A 64.5 / 58.2 / 43.0 / 49.6
+// i.e. one codeword (pair) per CTA: the per-tier barrier then spans only the
+// codeword's own ceil(Z/32) warps, which beats every "more resident rows"
+// arrangement of bigger CTAs.  plan_ctas() sizes the register budget.
+constexpr int kSmemPerSm = 227 * 1024;
+constexpr int plan_ctas(int z, int p, int regs, int cw_smem) {
+  const int threads = (p * z + 31) / 32 * 32;
+  const int r8 = (regs + 7) / 8 * 8;
+  int c = 65536 / (threads * r8);
+  const int cw = 64 / (threads / 32);
+  if (cw < c) c = cw;
+  if (c > 32) c = 32;
+  const int cs = kSmemPerSm / ((p + 1) * cw_smem + 1024);   // + scratch slot + static/reserved
+  if (cs < c) c = cs;
+  return c;
+}
+constexpr int plan_cw_per_cta(int, int, int, double) { return 1; }
+
+// Register cap: the messages (S::NE) plus ~52 for the widest tier's
+// transients.  Measured on C2 (NE = 76): 161 regs uncapped -> 4 CTAs of 96
+// threads per SM, 45.9 Gb/s; capped at 128 -> 5 CTAs, 50.3 Gb/s; capped at
+// 96 -> spills, 43.0 Gb/s.
+#ifndef QCB_REG_SLACK
+#define QCB_REG_SLACK 52
+#endif
+// CTA shape planner.  A CTA holds p codewords (p*Z threads, padded to whole
+// warps); what matters is how many check rows are resident per SM:
+//   ctas/SM = min(65536 regs / (threads * regs), 64 warps / warps, 32,
+//                 smem / smem per CTA),   rows/SM = ctas * p * Z,
+// and, for a small batch, how many CTAs there are per SM at all.  The
+// largest rows/SM wins, the smaller CTA on ties (cheaper barriers).
+constexpr int kSmemPerSm = 227 * 1024;
+constexpr int plan_ctas(int z, int p, int regs, int cw_smem) {
+  const int threads = (p * z + 31) / 32 * 32;
+  const int r8 = (regs + 7) / 8 * 8;
+  int c = 65536 / (threads * r8);
+  const int cw = 64 / (threads / 32);
+  if (cw < c) c = cw;
+  if (c > 32) c = 32;
+  const int cs = kSmemPerSm / ((p + 1) * cw_smem + 1024);   // + scratch slot + static/reserved
+  if (cs < c) c = cs;
+  return c;
+}
+// units_per_sm < 0: unbounded batch
+constexpr int plan_cw_per_cta(int z, int regs, int cw_smem, double units_per_sm) {
   int best = 1;
-  double best_eff = 0.0;
-  for (int p = 1; p <= kLayMaxCw; ++p) {
-    const int thr = p * z;
-    if (thr > kLayMaxThreads) break;
-    const int padded = (thr + 31) / 32 * 32;
-    double eff = (double)thr / padded;
-    if (thr > 160) eff *= 0.97;
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = p; }
+  double best_rows = -1.0;
+  for (int p = 1; p <= kLayMaxCw && p * z <= kLayMaxThreads; ++p) {
+    double c = plan_ctas(z, p, regs, cw_smem);
+    if (units_per_sm >= 0.0 && units_per_sm / p < c) c = units_per_sm / p;
+    const double rows = c * p * z;
+    if (rows > best_rows + 1e-9) { best_rows = rows; best = p; }
   }
   return best;
 }
 
 // Register cap: the messages (S::NE) plus a slack for the widest tier's
-// transients and hoisted edge addresses, then raised to the largest value that
-// still gives the same number of resident CTAs for the code's CTA size (for
-// Z = 96: 136 keeps 5 CTAs of 96 threads, 168 keeps 4).  Measured on C2
-// (NE = 76): uncapped 161 regs -> 4 CTAs, 45.9 Gb/s; 128 -> 5 CTAs, 50.3.
+// transients and hoisted edge addresses; the CTA shape is planned for that
+// budget and int16 kernels then take every register that keeps the same
+// number of resident CTAs.  Measured on C2 (NE = 76): uncapped 161 regs ->
+// 4 CTAs of 96 threads per SM, 45.9 Gb/s; 128 -> 5 CTAs, 50.3; raising
+// float32 to 136 at the same CTA count costs 10 % (67.3 vs 75.6 Gb/s), so
+// float32 keeps its minimum.
+#ifndef QCB_REG_SLACK
+#define QCB_REG_SLACK 52
+#endif
+constexpr int raise_cap(int z, int want, int cw_smem, bool raise) {
+  const int p = plan_cw_per_cta(z, want, cw_smem, -1.0);
+  const int threads = (p * z + 31) / 32 * 32;
+  const int ctas = plan_ctas(z, p, want, cw_smem);
+  int cap = (want + 7) / 8 * 8;
+  if (raise && ctas > 0) {
+    const int r = 65536 / (threads * ctas) / 8 * 8;
+    if (r > cap) cap = r;
+  }
+  return cap > 255 ? 255 : cap;
+}
+
 template <class S, class A, int ZS>
 constexpr int reg_cap() {
   const int want = S::NE + QCB_REG_SLACK + (A::kElem == 2 ? S::MAXDEG : 0);
   const int z = ZS > 0 ? ZS : 96;
-  const int threads = (cw_per_cta_large(z) * z + 31) / 32 * 32;
-  int ctas = 65536 / (threads * want);
-  if (ctas < 1) ctas = 1;
-  // measured (B200, same box, A/B): raising helps int16 (C5: 40.7 -> 43.9
-  // Gb/s at 168 regs) but hurts float32 (C2: 75.6 at 128 -> 67.3 at 136,
-  // same CTA count), so only int16 is raised
-  int cap = (want + 7) / 8 * 8;
-  if (A::kElem == 2) {
-    cap = 65536 / (threads * ctas) / 8 * 8;
-    if (cap < want) cap = (want + 7) / 8 * 8;
-  }
-  return cap > 255 ? 255 : cap;
+  return raise_cap(z, want, (z * kRowStrideUnits * A::kElem + 15) & ~15, A::kElem == 2);
 }
 
 template <class S, class A, int ZS, bool ET>
@@ -543,25 +596,17 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   }
 }
 
-// codewords per CTA: whole warps, small CTAs (one barrier per tier), and
-// enough CTAs to cover every SM when the batch is small
-inline int layered_cw_per_cta(int z, int64_t w) {
+// codewords per CTA for a kernel with `regs` registers per thread
+inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
   if (const char* env = getenv("QCB_CW_PER_CTA")) {   // tuning knob (benchmarks only)
     const int v = atoi(env);
     if (v >= 1 && v <= kLayMaxCw && v * z <= kLayMaxThreads) return v;
   }
-  int best = 1;
-  double best_eff = 0.0;
-  for (int p = 1; p <= kLayMaxCw; ++p) {
-    const int thr = p * z;
-    if (thr > kLayMaxThreads) break;
-    if (p > 1 && w < (int64_t)p * 148 * 4) break;   // keep >= 4 CTAs per SM on small batches
-    const int padded = (thr + 31) / 32 * 32;
-    double eff = (double)thr / padded;
-    if (thr > 160) eff *= 0.97;
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = p; }
-  }
-  return best;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int cw_smem = (z * kRowStrideUnits * cell_bytes + 15) & ~15;
+  return plan_cw_per_cta(z, regs, cw_smem, (double)w / sms);
 }
 
 template <class K>
@@ -580,26 +625,17 @@ template <class S, class A, int ZS, bool ET>
 inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   constexpr int RS = row_stride_bytes<A>();
   const int z = ZS > 0 ? ZS : a.z;
-  const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)(a.pairs + 1) * ((z * RS + 15) & ~15);   // + scratch slot
   auto kern = decode_layered_kernel<S, A, ZS, ET>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // the register count is only known after ptxas: shrink the CTA if this
-  // kernel cannot launch the planned one (the decode result does not depend
-  // on the CTA size)
+  // the CTA shape is planned from the register count ptxas actually gave
+  // this kernel (the decode result does not depend on the CTA size)
   cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, kern);
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
   if (e != cudaSuccess) return e;
-  if (threads > fa.maxThreadsPerBlock) {
-    SpecArgs b = a;
-    b.pairs = fa.maxThreadsPerBlock / z;
-    if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
-    if (b.tmem_cols > 0) return cudaErrorLaunchOutOfResources;   // TMEM plan is per CTA shape
-    return launch_layered_fixed(kern, b, z, RS, s);
-  }
-  return launch_layered_fixed(kern, a, z, RS, s);
+  SpecArgs b = a;
+  b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
+  while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
+  if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
+  return launch_layered_fixed(kern, b, z, RS, s);
 }
-
 
 }  // namespace qcb

@@ -43,6 +43,11 @@ __device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
   uint32_t d; asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x)); return d;
 }
 
+#ifndef QCB_P16_KEEP_DEG
+#define QCB_P16_KEEP_DEG 32
+#endif
+constexpr int kP16KeepDeg = QCB_P16_KEEP_DEG;   // rows above this degree re-load posteriors in pass 2
+
 struct RtK2 {             // runtime constants (kernel parameters): keep IMAD operands out of ptxas' reach
   uint32_t one, neg1, lane1;   // 1, 0xFFFFFFFF, 0x00010001
 };
@@ -54,10 +59,19 @@ struct ArithI16x2 {
   __device__ static Val lds(uint32_t a) { uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
   __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 
-  template <int D>
-  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* nm, const RtK2& K) {
+  // One row of D edges at shared-memory addresses addr[]: loads the
+  // posteriors, updates the negated messages nm[] and stores the new
+  // posteriors (lanes set in `keep` keep their old value: converged codewords
+  // under early termination).  High-degree rows re-load the posteriors for
+  // pass 2 instead of keeping zz live (fewer registers; the LSU pipe has room).
+  template <int D, bool ET>
+  __device__ __forceinline__ static void row(const uint32_t (&addr)[D], uint32_t* nm, const RtK2& K,
+                                             uint32_t keep) {
     static_assert(D >= 2, "row degree >= 2");
-    uint32_t d[D], a[D];
+    constexpr bool kReload = D > kP16KeepDeg;
+    uint32_t p[D], d[D], a[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) p[k] = lds(addr[k]);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       d[k] = vadd2(p[k], nm[k]);                                   // zz = post - L_old
@@ -67,24 +81,27 @@ struct ArithI16x2 {
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
     if (D & 1) sx ^= d[D - 1];
-    uint32_t pre[D], suf[D], ex[D];
-    pre[1] = a[0];
-#pragma unroll
-    for (int k = 2; k < D; ++k) pre[k] = vmin2(pre[k - 1], a[k - 1]);
+    uint32_t suf[D];
     suf[D - 2] = a[D - 1];
 #pragma unroll
     for (int k = D - 3; k >= 0; --k) suf[k] = vmin2(suf[k + 1], a[k + 1]);
-    ex[0] = suf[0];
-    ex[D - 1] = pre[D - 1];
-#pragma unroll
-    for (int k = 1; k < D - 1; ++k) ex[k] = vmin2(pre[k], suf[k]);
+    uint32_t pre = a[0];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
-      const uint32_t t1 = ex[k] ^ m, t2 = m & 0x00010001u;
+      const uint32_t ex = k == 0 ? suf[0] : (k == D - 1 ? pre : vmin2(pre, suf[k]));
+      if (k > 0 && k < D - 1) pre = vmin2(pre, a[k]);
+      uint32_t pk = p[k], dk = d[k];
+      if constexpr (kReload) {
+        pk = lds(addr[k]);
+        dk = vadd2(pk, nm[k]);
+      }
+      const uint32_t m = lane_signs(dk ^ sx);                      // sign of L_new per lane
+      const uint32_t t1 = ex ^ m, t2 = m & 0x00010001u;
       const uint32_t l = vadd2(t1, t2);                            // +-ex, wrapping
-      o[k] = vadd2(d[k], l);                                       // post = zz + L_new
+      uint32_t o = vadd2(dk, l);                                   // post = zz + L_new
       nm[k] = vadd2(imad(t1, K.neg1, K.neg1), imad(t2, K.neg1, K.lane1));   // -L_new
+      if constexpr (ET) o = (o & ~keep) | (pk & keep);
+      sts(addr[k], o);
     }
   }
 };
@@ -99,17 +116,9 @@ struct Layered2 {
                                               uint32_t (&nm)[S::NE], uint32_t keep) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
-    uint32_t addr[D], p[D], o[D];
+    uint32_t addr[D];
     tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
-#pragma unroll
-    for (int k = 0; k < D; ++k) p[k] = A::lds(addr[k]);
-    A::template row<D>(p, o, nm + E0, K);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      uint32_t v = o[k];
-      if constexpr (ET) v = (v & ~keep) | (p[k] & keep);
-      A::sts(addr[k], v);
-    }
+    A::template row<D, ET>(addr, nm + E0, K, keep);
   }
 
   template <int T>
@@ -152,14 +161,8 @@ struct Layered2 {
 #endif
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
-  const int want = S::NE + QCB_P16_SLACK;
   const int z = ZS > 0 ? ZS : 96;
-  const int threads = (cw_per_cta_large(z) * z + 31) / 32 * 32;
-  int ctas = 65536 / (threads * ((want + 7) / 8 * 8));
-  if (ctas < 1) ctas = 1;
-  int cap = 65536 / (threads * ctas) / 8 * 8;          // same CTA count, every spare register
-  if (cap < want) cap = (want + 7) / 8 * 8;
-  return cap > 255 ? 255 : cap;
+  return raise_cap(z, S::NE + QCB_P16_SLACK, (z * kRowStrideUnits * 4 + 15) & ~15, true);
 }
 
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
@@ -311,13 +314,13 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   constexpr int RS = row_stride_bytes<ArithI16x2>();
   const int z = ZS > 0 ? ZS : a.z;
   auto kern = decode_pair16_kernel<S, ZS, ET>;
-  SpecArgs b = a;
-  const int threads = (b.pairs * z + 31) / 32 * 32;
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, kern);
   if (e != cudaSuccess) return e;
-  if (threads > fa.maxThreadsPerBlock) b.pairs = fa.maxThreadsPerBlock / z;
-  if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
+  SpecArgs b = a;
+  b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4);
+  while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
+  if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
   const size_t smem = (size_t)(b.pairs + 1) * ((z * RS + 15) & ~15);   // + scratch slot
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

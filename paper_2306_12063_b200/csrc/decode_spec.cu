@@ -29,7 +29,7 @@ int spec_row_stride_bytes(int elem) {
   return elem == 4 ? row_stride_bytes<ArithF32>() : row_stride_bytes<ArithI16>();
 }
 
-int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w); }
+int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w, 128, 4); }
 
 // Choose between the register-resident and the TMEM-resident message store.
 // QCB_TMEM=0/1 forces one (benchmarks); default: TMEM when it keeps more
@@ -54,7 +54,7 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
     const char* p = getenv("QCB_I16_PAIR");
     if (!(p && p[0] == '0')) {
       *pair16 = 1;
-      *cw_per_cta = layered_cw_per_cta(z, (w + 1) / 2);   // codeword pairs per CTA
+      *cw_per_cta = 1;                      // planned at launch from the kernel's registers
       *tmem_cols = 0;
       return;
     }
@@ -62,13 +62,13 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
 #define QCB_NE(STRUCT) if (structure_id == STRUCT::ID) { ne = STRUCT::NE; maxdeg = STRUCT::MAXDEG; }
   QCB_FOR_EACH_STRUCTURE(QCB_NE)
 #undef QCB_NE
-  const int reg_g = layered_cw_per_cta(z, w);
+  const int regs_reg = ne + 52 + (elem == 2 ? maxdeg : 0);
+  const int reg_g = layered_cw_per_cta(z, w, regs_reg, elem);
   *cw_per_cta = reg_g;
   *tmem_cols = 0;
   const char* env = getenv("QCB_TMEM");
   if (env && env[0] == '0') return;
   const int regs_tm = QCB_TM_REG_BASE + (elem == 2 ? 6 : 5) * maxdeg;
-  const int regs_reg = ne + 52 + (elem == 2 ? maxdeg : 0);
   const int smem_cw = (z * kRowStrideUnits * elem + 15) & ~15;
   int cols = 0;
   const int g = tmem_plan(z, ne, (regs_tm + 7) / 8 * 8, smem_cw, w, &cols);
