@@ -356,13 +356,6 @@ struct Layered {
   }
 };
 
-// Register cap: the messages (S::NE) plus ~52 for the widest tier's
-// transients.  Measured on C2 (NE = 76): 161 regs uncapped -> 4 CTAs of 96
-// threads per SM, 45.9 Gb/s; capped at 128 -> 5 CTAs, 50.3 Gb/s; capped at
-// 96 -> spills, 43.0 Gb/s.
-#ifndef QCB_REG_SLACK
-#define QCB_REG_SLACK 52
-#endif
 // CTA shape.  A CTA holds p codewords (p*Z threads, padded to whole warps).
 // Measured on B200 (tools/exp/ctasweep.py, 16384 f32 / 65536 int16
 // codewords, 10 iterations), coded Gbit/s for p = 1 / 2 / 3 / 4:
@@ -388,44 +381,6 @@ constexpr int plan_ctas(int z, int p, int regs, int cw_smem) {
   return c;
 }
 constexpr int plan_cw_per_cta(int, int, int, double) { return 1; }
-
-// Register cap: the messages (S::NE) plus ~52 for the widest tier's
-// transients.  Measured on C2 (NE = 76): 161 regs uncapped -> 4 CTAs of 96
-// threads per SM, 45.9 Gb/s; capped at 128 -> 5 CTAs, 50.3 Gb/s; capped at
-// 96 -> spills, 43.0 Gb/s.
-#ifndef QCB_REG_SLACK
-#define QCB_REG_SLACK 52
-#endif
-// CTA shape planner.  A CTA holds p codewords (p*Z threads, padded to whole
-// warps); what matters is how many check rows are resident per SM:
-//   ctas/SM = min(65536 regs / (threads * regs), 64 warps / warps, 32,
-//                 smem / smem per CTA),   rows/SM = ctas * p * Z,
-// and, for a small batch, how many CTAs there are per SM at all.  The
-// largest rows/SM wins, the smaller CTA on ties (cheaper barriers).
-constexpr int kSmemPerSm = 227 * 1024;
-constexpr int plan_ctas(int z, int p, int regs, int cw_smem) {
-  const int threads = (p * z + 31) / 32 * 32;
-  const int r8 = (regs + 7) / 8 * 8;
-  int c = 65536 / (threads * r8);
-  const int cw = 64 / (threads / 32);
-  if (cw < c) c = cw;
-  if (c > 32) c = 32;
-  const int cs = kSmemPerSm / ((p + 1) * cw_smem + 1024);   // + scratch slot + static/reserved
-  if (cs < c) c = cs;
-  return c;
-}
-// units_per_sm < 0: unbounded batch
-constexpr int plan_cw_per_cta(int z, int regs, int cw_smem, double units_per_sm) {
-  int best = 1;
-  double best_rows = -1.0;
-  for (int p = 1; p <= kLayMaxCw && p * z <= kLayMaxThreads; ++p) {
-    double c = plan_ctas(z, p, regs, cw_smem);
-    if (units_per_sm >= 0.0 && units_per_sm / p < c) c = units_per_sm / p;
-    const double rows = c * p * z;
-    if (rows > best_rows + 1e-9) { best_rows = rows; best = p; }
-  }
-  return best;
-}
 
 // Register cap: the messages (S::NE) plus a slack for the widest tier's
 // transients and hoisted edge addresses; the CTA shape is planned for that
