@@ -111,6 +111,38 @@ int qc_decode_batch_i16_host(const int32_t* row_ptr, int64_t row_ptr_len, const 
 int qc_encode_packed(qc_code_t code, const uint8_t* info, int64_t w, uint8_t* cw, void* cuda_stream);
 int qc_encode_packed_host(qc_code_t code, const uint8_t* info, int64_t w, uint8_t* cw);
 
+/* ---- channel, waterfall counters and decode records -------
+ * All pointers device memory, stream ordered.
+ *
+ * qc_encode_array   <- encoder.encode_array (encoder.py:133-163): one bit per
+ *   byte, any Z (the packed encoder needs Z % 8 == 0).  w x K in, w x N out.
+ * qc_frames_info    <- chansim._gen_batch's info bits (chansim.py:126-133),
+ *   drawn from a device Philox4x32-10 stream keyed by (seed, point, frame):
+ *   independent of launch shape and GPU count, NOT numpy's stream.
+ * qc_channel_llr    <- chansim._llr_batch (chansim.py:136-143): BPSK, AWGN,
+ *   LLR = (2/sigma2) y cast to float32 and, for q_b > 0, quantize_llr
+ *   (decoder.py:165-171) to int16.  noise != NULL: the caller's float64
+ *   standard normal samples (bit-exact with the reference for the same
+ *   samples); noise == NULL: device Philox noise for frames frame0.. .
+ * qc_quantize_llr   <- decoder.quantize_llr on float32 LLRs.
+ * qc_count_errors   <- run_waterfall's counting (chansim.py:166-171): per
+ *   `batch` consecutive frames, {bit errors over the K info bits, frame
+ *   errors, iteration sum} as uint64 triples (zeroed by the call).
+ * qc_pack_records   <- the CLI decode output (cli.py:180-183): per codeword
+ *   ceil(N/8) packed hard bytes, min(iters, 255), converged.
+ */
+int qc_encode_array(qc_code_t code, const uint8_t* info_bits, int64_t w, uint8_t* cw_bits, void* cuda_stream);
+int qc_frames_info(uint64_t seed, uint32_t point, int64_t frame0, int64_t w, int32_t k, uint8_t* info_bits,
+                   void* cuda_stream);
+int qc_channel_llr(const uint8_t* cw_bits, int64_t w, int32_t n, double sigma2, const double* noise,
+                   uint64_t seed, uint32_t point, int64_t frame0, int32_t q_b, double l_clip, void* llr,
+                   void* cuda_stream);
+int qc_quantize_llr(const float* x, int64_t count, int32_t q_b, double l_clip, int16_t* out, void* cuda_stream);
+int qc_count_errors(const uint8_t* hard, int32_t hard_packed, const uint8_t* info_bits, const int32_t* iters,
+                    int64_t w, int32_t n, int32_t k, int32_t batch, uint64_t* batch_sums, void* cuda_stream);
+int qc_pack_records(const uint8_t* hard_packed, const int32_t* iters, const uint8_t* conv, int64_t w, int32_t n,
+                    uint8_t* records, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

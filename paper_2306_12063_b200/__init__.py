@@ -24,4 +24,10 @@ from .errors import (ArithmeticMismatch, BadZ, CodecError, CorruptFile,
                      NativeLibraryError, SizeMismatch, UnsupportedCode,
                      UnsupportedZ)
 
-__version__ = "0.1.0"
+from . import channel, llrio  # noqa: E402  (device channel / waterfall, LLR0 + records)
+from .channel import (ChannelConfig, ThroughputReport, WaterfallPoint,
+                      WaterfallTable, ebn0_to_sigma2, run_throughput_bench,
+                      run_waterfall)
+from .llrio import decode_llr_file, read_llr_file, write_llr_file
+
+__version__ = "0.2.0"

@@ -6,6 +6,7 @@
 // data.  Outputs are caller-owned, exactly like the reference kernel boundary
 // (_kernels.py:17-19: hard/iters/conv are written in place).
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -301,7 +302,7 @@ int decode_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_
 
 extern "C" {
 
-int qc_version(void) { return 100; }
+int qc_version(void) { return 110; }
 const char* qc_last_error(void) { return g_err.c_str(); }
 
 int qc_code_create(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code_t* out) {
@@ -433,6 +434,91 @@ int qc_encode_packed_host(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* 
   cudaFree(d_out);
   if (rc) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "encode_packed (host path)");
+  return QC_OK;
+}
+
+// ---- channel, waterfall counters, records --------------------------
+
+int qc_encode_array(qc_code_t c, const uint8_t* info_bits, int64_t w, uint8_t* cw_bits, void* stream) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (c->enc_y < 0) return fail(QC_EMALFORMED, "h_b column lacks a single interior entry");
+  if (c->mb > 12 || c->nb > 24 || c->mb < 2) return fail(QC_EUNSUPPORTED, "encoder supports 2<=mb<=12, nb<=24");
+  if (w < 0) return fail(QC_EINVAL, "w < 0");
+  if (w == 0) return QC_OK;
+  if (!info_bits || !cw_bits) return fail(QC_EINVAL, "NULL buffer");
+  EncodeArgs a;
+  memset(&a, 0, sizeof a);
+  a.info = info_bits; a.cw = cw_bits; a.w = w; a.mb = c->mb; a.nb = c->nb; a.z = c->z; a.hb_shift = c->enc_hb;
+  for (int i = 0; i < c->mb * c->nb; ++i) a.shifts[i] = c->shifts[i];
+  cudaError_t e = launch_encode_array(a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "encode_array");
+  return QC_OK;
+}
+
+int qc_frames_info(uint64_t seed, uint32_t point, int64_t frame0, int64_t w, int32_t k, uint8_t* info_bits,
+                   void* stream) {
+  if (w < 0 || k < 0 || frame0 < 0) return fail(QC_EINVAL, "negative size");
+  if (w == 0 || k == 0) return QC_OK;
+  if (!info_bits) return fail(QC_EINVAL, "NULL buffer");
+  cudaError_t e = launch_frames_info(seed, point, frame0, w, k, info_bits, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "frames_info");
+  return QC_OK;
+}
+
+int qc_channel_llr(const uint8_t* cw_bits, int64_t w, int32_t n, double sigma2, const double* noise,
+                   uint64_t seed, uint32_t point, int64_t frame0, int32_t q_b, double l_clip, void* llr,
+                   void* stream) {
+  if (!(sigma2 > 0.0)) return fail(QC_EINVAL, "sigma2 = %g (must be > 0, chansim.py:59-60)", sigma2);
+  if (w < 0 || n < 0 || (n & 1) || frame0 < 0) return fail(QC_EINVAL, "bad shape w=%lld n=%d", (long long)w, n);
+  if (q_b < 0 || q_b > 14) return fail(QC_EINVAL, "q_b must stay in [1, 14] (0 = float32 out)");
+  if (q_b > 0 && !(l_clip > 0.0)) return fail(QC_EINVAL, "l_clip must be > 0");
+  if (w == 0 || n == 0) return QC_OK;
+  if (!cw_bits || !llr) return fail(QC_EINVAL, "NULL buffer");
+  ChannelArgs a;
+  memset(&a, 0, sizeof a);
+  a.bits = cw_bits; a.noise = noise; a.llr = llr; a.w = w; a.n = n;
+  a.seed = seed; a.point = point; a.frame0 = frame0;
+  a.sqrt_sigma2 = std::sqrt(sigma2);
+  a.two_over_sigma2 = 2.0 / sigma2;
+  if (q_b > 0) {
+    const double lim = (double)((1 << q_b) - 1);
+    a.q_lim = lim;
+    a.q_scale = lim / l_clip;
+  }
+  cudaError_t e = launch_channel(a, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "channel_llr");
+  return QC_OK;
+}
+
+int qc_quantize_llr(const float* x, int64_t count, int32_t q_b, double l_clip, int16_t* out, void* stream) {
+  if (q_b < 1 || q_b > 14) return fail(QC_EINVAL, "q_b must stay in [1, 14] (decoder.py:167-168)");
+  if (!(l_clip > 0.0)) return fail(QC_EINVAL, "l_clip must be > 0");
+  if (count < 0) return fail(QC_EINVAL, "count < 0");
+  if (count == 0) return QC_OK;
+  if (!x || !out) return fail(QC_EINVAL, "NULL buffer");
+  const double lim = (double)((1 << q_b) - 1);
+  cudaError_t e = launch_quantize(x, count, lim / l_clip, lim, out, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "quantize_llr");
+  return QC_OK;
+}
+
+int qc_count_errors(const uint8_t* hard, int32_t hard_packed, const uint8_t* info_bits, const int32_t* iters,
+                    int64_t w, int32_t n, int32_t k, int32_t batch, uint64_t* batch_sums, void* stream) {
+  if (w < 0 || n <= 0 || k < 0 || k > n || batch < 1) return fail(QC_EINVAL, "bad shape");
+  if (!hard || !info_bits || !iters || !batch_sums) return fail(QC_EINVAL, "NULL buffer");
+  cudaError_t e = launch_count_errors(hard, hard_packed ? 1 : 0, info_bits, iters, w, n, k, batch,
+                                      reinterpret_cast<unsigned long long*>(batch_sums), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "count_errors");
+  return QC_OK;
+}
+
+int qc_pack_records(const uint8_t* hard_packed, const int32_t* iters, const uint8_t* conv, int64_t w, int32_t n,
+                    uint8_t* records, void* stream) {
+  if (w < 0 || n <= 0) return fail(QC_EINVAL, "bad shape");
+  if (w == 0) return QC_OK;
+  if (!hard_packed || !iters || !conv || !records) return fail(QC_EINVAL, "NULL buffer");
+  cudaError_t e = launch_pack_records(hard_packed, iters, conv, w, (n + 7) / 8, records, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack_records");
   return QC_OK;
 }
 

@@ -66,4 +66,28 @@ struct EncodeArgs {
 // structure_id: index into kStructureMasks, -1 = generic
 cudaError_t launch_encode_packed(const EncodeArgs& a, int structure_id, cudaStream_t s);
 
+// ---- channel / waterfall / records (channel.cu) -----------------------------------
+struct ChannelArgs {
+  const uint8_t* bits;     // W x N codeword bits, one per byte
+  const double* noise;     // W x N standard normal samples, or NULL: device Philox stream
+  void* llr;               // W x N float32 (q_lim == 0) or int16
+  int64_t w;
+  int32_t n;
+  uint32_t point;
+  int64_t frame0;
+  uint64_t seed;
+  double sqrt_sigma2, two_over_sigma2;   // math.sqrt(sigma2), 2.0 / sigma2 (host-computed, as the reference)
+  double q_scale, q_lim;                 // lim / l_clip and lim (q_lim == 0: float32 LLRs out)
+};
+cudaError_t launch_frames_info(uint64_t seed, uint32_t point, int64_t frame0, int64_t w, int32_t k, uint8_t* info,
+                               cudaStream_t s);
+cudaError_t launch_encode_array(const EncodeArgs& a, cudaStream_t s);
+cudaError_t launch_channel(const ChannelArgs& a, cudaStream_t s);
+cudaError_t launch_quantize(const float* x, int64_t count, double scale, double lim, int16_t* out, cudaStream_t s);
+cudaError_t launch_count_errors(const uint8_t* hard, int32_t packed, const uint8_t* info, const int32_t* iters,
+                                int64_t w, int32_t n, int32_t k, int32_t batch, unsigned long long* sums,
+                                cudaStream_t s);
+cudaError_t launch_pack_records(const uint8_t* hard_packed, const int32_t* iters, const uint8_t* conv, int64_t w,
+                                int32_t nbytes, uint8_t* out, cudaStream_t s);
+
 }  // namespace qcb

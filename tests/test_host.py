@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     L = _lib.lib()
     for name in declared:
         assert hasattr(L, name), name
-    assert L.qc_version() == 100
+    assert L.qc_version() == 110
 
 
 def test_code_handles_without_gpu():
