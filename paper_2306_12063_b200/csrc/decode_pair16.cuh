@@ -20,8 +20,8 @@
 //           a = max(d, ~d + 0x10001) = |d| (wrapping)    (IMAD, VIADD, VIMNMX)
 //   minima  ex_k = min_{j != k} a_j (prefix / suffix)    (VIMNMX)
 //   pass 2  m    = lane sign mask of d ^ parity          (LOP3, PRMT)
-//           L    = (ex ^ m) + (m & 0x10001)  = +-ex      (LOP3, LOP3, VIADD)
-//           post = d + L, nm = ~(ex ^ m) + (0x10001 - (m & 0x10001))
+//           nex  = ~ex + 0x10001 = -ex                   (IMAD, VIADD)
+//           post = d + (m ? nex : ex), nm = m ? ex : nex (LOP3, VIADD, LOP3)
 // Shared memory layout, addressing and tier schedule are the float32
 // kernel's (4-byte cells, decode_layered.cuh).
 #pragma once
@@ -96,10 +96,9 @@ struct ArithI16x2 {
         dk = vadd2(pk, nm[k]);
       }
       const uint32_t m = lane_signs(dk ^ sx);                      // sign of L_new per lane
-      const uint32_t t1 = ex ^ m, t2 = m & 0x00010001u;
-      const uint32_t l = vadd2(t1, t2);                            // +-ex, wrapping
-      uint32_t o = vadd2(dk, l);                                   // post = zz + L_new
-      nm[k] = vadd2(imad(t1, K.neg1, K.neg1), imad(t2, K.neg1, K.lane1));   // -L_new
+      const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
+      uint32_t o = vadd2(dk, (nex & m) | (ex & ~m));               // post = zz + L_new
+      nm[k] = (ex & m) | (nex & ~m);                               // -L_new
       if constexpr (ET) o = (o & ~keep) | (pk & keep);
       sts(addr[k], o);
     }
