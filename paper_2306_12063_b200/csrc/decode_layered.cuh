@@ -88,7 +88,7 @@ __device__ __forceinline__ void f_add2(float a0, float a1, float b0, float b1, f
 }
 
 struct RtK {              // runtime constants (kernel parameters)
-  uint32_t one, sign, shr, neg1;
+  uint32_t one, sign, shr, neg1, lane1;   // lane1 = 0x00010001 (16x2 kernels)
 };
 
 // ---------------------------------------------------------------------------
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   __shared__ int s_fail[kLayMaxCw], s_done[kLayMaxCw], s_iters[kLayMaxCw];
   __shared__ int s_active;
 
-  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1};
+  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
   const int N = S::NB * Z;
   const int G = a.pairs;                        // codewords per CTA

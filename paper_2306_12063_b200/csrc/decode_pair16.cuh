@@ -43,15 +43,6 @@ __device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
   uint32_t d; asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x)); return d;
 }
 
-#ifndef QCB_P16_KEEP_DEG
-#define QCB_P16_KEEP_DEG 32
-#endif
-constexpr int kP16KeepDeg = QCB_P16_KEEP_DEG;   // rows above this degree re-load posteriors in pass 2
-
-struct RtK2 {             // runtime constants (kernel parameters): keep IMAD operands out of ptxas' reach
-  uint32_t one, neg1, lane1;   // 1, 0xFFFFFFFF, 0x00010001
-};
-
 struct ArithI16x2 {
   using Val = uint32_t;
   static constexpr int kElem = 4;        // one cell = the two codewords' int16 posteriors
@@ -59,19 +50,12 @@ struct ArithI16x2 {
   __device__ static Val lds(uint32_t a) { uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
   __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
 
-  // One row of D edges at shared-memory addresses addr[]: loads the
-  // posteriors, updates the negated messages nm[] and stores the new
-  // posteriors (lanes set in `keep` keep their old value: converged codewords
-  // under early termination).  High-degree rows re-load the posteriors for
-  // pass 2 instead of keeping zz live (fewer registers; the LSU pipe has room).
-  template <int D, bool ET>
-  __device__ __forceinline__ static void row(const uint32_t (&addr)[D], uint32_t* nm, const RtK2& K,
-                                             uint32_t keep) {
+  // One row of D edges: posteriors p[] in, new posteriors o[] out, negated
+  // messages nm[] updated in place (both codewords' lanes).
+  template <int D>
+  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* nm, const RtK& K) {
     static_assert(D >= 2, "row degree >= 2");
-    constexpr bool kReload = D > kP16KeepDeg;
-    uint32_t p[D], d[D], a[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) p[k] = lds(addr[k]);
+    uint32_t d[D], a[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       d[k] = vadd2(p[k], nm[k]);                                   // zz = post - L_old
@@ -90,17 +74,10 @@ struct ArithI16x2 {
     for (int k = 0; k < D; ++k) {
       const uint32_t ex = k == 0 ? suf[0] : (k == D - 1 ? pre : vmin2(pre, suf[k]));
       if (k > 0 && k < D - 1) pre = vmin2(pre, a[k]);
-      uint32_t pk = p[k], dk = d[k];
-      if constexpr (kReload) {
-        pk = lds(addr[k]);
-        dk = vadd2(pk, nm[k]);
-      }
-      const uint32_t m = lane_signs(dk ^ sx);                      // sign of L_new per lane
+      const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
       const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
-      uint32_t o = vadd2(dk, (nex & m) | (ex & ~m));               // post = zz + L_new
+      o[k] = vadd2(d[k], (nex & m) | (ex & ~m));                   // post = zz + L_new
       nm[k] = (ex & m) | (nex & ~m);                               // -L_new
-      if constexpr (ET) o = (o & ~keep) | (pk & keep);
-      sts(addr[k], o);
     }
   }
 };
@@ -111,13 +88,21 @@ struct Layered2 {
 
   // keep: lanes of converged codewords (early termination) keep their posteriors
   template <int T, bool ET>
-  __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK2& K, int r, uint32_t b0, uint32_t b1,
+  __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
                                               uint32_t (&nm)[S::NE], uint32_t keep) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
-    uint32_t addr[D];
+    uint32_t addr[D], p[D], o[D];
     tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
-    A::template row<D, ET>(addr, nm + E0, K, keep);
+#pragma unroll
+    for (int k = 0; k < D; ++k) p[k] = A::lds(addr[k]);
+    A::template row<D>(p, o, nm + E0, K);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      uint32_t v = o[k];
+      if constexpr (ET) v = (v & ~keep) | (p[k] & keep);       // converged lanes keep their posteriors
+      A::sts(addr[k], v);
+    }
   }
 
   template <int T>
@@ -137,7 +122,7 @@ struct Layered2 {
   }
 
   template <bool ET, int... Ts>
-  __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK2& K, int r, uint32_t b0, uint32_t b1,
+  __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
                                                uint32_t (&nm)[S::NE], bool work, uint32_t keep,
                                                std::integer_sequence<int, Ts...>) {
     if constexpr (ET) {
@@ -175,7 +160,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
   __shared__ int s_active;
 
-  const RtK2 K{a.k_one, a.k_neg1, a.k_lane1};
+  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
   const int N = S::NB * Z;
   const int G = a.pairs;

@@ -50,6 +50,7 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
                int32_t* pair16) {
   int ne = 0, maxdeg = 0;
   *pair16 = 0;
+
   if (elem == 2) {                          // int16: two codewords per thread in 16x2 lanes
     const char* p = getenv("QCB_I16_PAIR");
     if (!(p && p[0] == '0')) {

@@ -110,6 +110,7 @@ struct LayeredTm {
     constexpr int TN = (T + 1) % S::MB;
     uint32_t* cur = (T & 1) ? bufB : bufA;
     uint32_t* nxt = (T & 1) ? bufA : bufB;
+    tm_wait_st();                                // previous tier's store (issued a tier ago)
     tm_wait_ld<D>(cur);
     tm_ld_n<S::START[TN], S::DEG[TN]>(tb, nxt);
     if (work) {
@@ -126,8 +127,7 @@ struct LayeredTm {
 #pragma unroll
       for (int k = 0; k < D; ++k) A::sts(addr[k], o[k]);
     }
-    tm_st_n<E0, D>(tb, cur);
-    tm_wait_st();
+    tm_st_n<E0, D>(tb, cur);                     // waited on at the start of the next tier
   }
 
   __device__ __forceinline__ static Val from_bits(uint32_t b) {
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   __shared__ int s_active;
   __shared__ uint32_t s_taddr;
 
-  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1};
+  const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
   const int N = S::NB * Z;
   const int G = a.pairs;
@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
     __syncthreads();
     if (!s_active) break;
   }
+  tm_wait_st();
   tm_wait_ld<S::DEG[0]>(bufA);                  // drain the last prefetch
 
   // ---- outputs ---------------------------------------------------------------------
