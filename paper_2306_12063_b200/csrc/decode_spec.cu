@@ -74,15 +74,12 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   int cols = 0;
   const int g = tmem_plan(z, ne, (regs_tm + 7) / 8 * 8, smem_cw, w, &cols);
   if (g <= 0) return;
-  const int warps_reg = (reg_g * z + 31) / 32;
-  const int reg_ctas = std::min(65536 / (warps_reg * 32 * ((regs_reg + 7) / 8 * 8)), 64 / warps_reg);
-  const int warps_tm = (g * z + 31) / 32;
-  const int tm_ctas = std::min(std::min(512 / cols, 65536 / (warps_tm * 32 * ((regs_tm + 7) / 8 * 8))), 64 / warps_tm);
-  // measured on B200 (round 1): TMEM-resident messages pay off for the
-  // high-degree codes (Wi-Fi 1944 R5/6 int16: +17 %) but cost 5-6 % on the
-  // degree-6/7 and degree-15 codes, where the register kernel already fits
-  // 4-5 codewords per SM and the extra tcgen05 ld/st per tier do not pay back
-  const bool prefer = maxdeg >= 18 && tm_ctas * g > reg_ctas * reg_g;
+  // measured on B200 (round 1, tools/exp/tmem_ab.py, f32 coded Gb/s register / TMEM):
+  // row degree 20 gains (Wi-Fi 1944 R5/6 43.2 / 46.5, WiMAX 2304 R5/6 52.7 / 55.8,
+  // WiMAX 1152 R5/6 34.7 / 43.7); degree 22 loses (Wi-Fi 648 R5/6 39.7 / 35.4,
+  // Wi-Fi 1296 R5/6 43.8 / 33.5) and so do the low-degree codes (5-6 %):
+  // TMEM reads (64 B/clk/SM) only pay where the register kernel is starved
+  const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20;
   if ((env && env[0] == '1') || prefer) {
     *cw_per_cta = g;
     *tmem_cols = cols;
