@@ -86,22 +86,32 @@ template <class S, int ZS>
 struct Layered2 {
   using A = ArithI16x2;
 
-  // keep: lanes of converged codewords (early termination) keep their posteriors
+  // keep: lanes of converged codewords (early termination) keep their posteriors;
+  // pe: this tier's early-loaded posteriors, pn: next tier's (early_edge)
   template <int T, bool ET>
   __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                              uint32_t (&nm)[S::NE], uint32_t keep) {
+                                              uint32_t (&nm)[S::NE], uint32_t keep, uint32_t (&pe)[S::MAXDEG],
+                                              uint32_t (&pn)[S::MAXDEG]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D], p[D], o[D];
     tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
-    for (int k = 0; k < D; ++k) p[k] = A::lds(addr[k]);
+    for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
     A::template row<D>(p, o, nm + E0, K);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       uint32_t v = o[k];
       if constexpr (ET) v = (v & ~keep) | (p[k] & keep);       // converged lanes keep their posteriors
       A::sts(addr[k], v);
+    }
+    if constexpr (T + 1 < S::MB) {
+      constexpr int DN = S::DEG[T + 1];
+      uint32_t an[DN];
+      tier_addrs<S, A, ZS, S::START[T + 1]>(a, r, b0, b1, an, std::make_integer_sequence<int, DN>{});
+#pragma unroll
+      for (int k = 0; k < DN; ++k)
+        if (early_edge<S, T + 1>(k)) pn[k] = A::lds(an[k]);
     }
   }
 
@@ -125,11 +135,13 @@ struct Layered2 {
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
                                                uint32_t (&nm)[S::NE], bool work, uint32_t keep,
                                                std::integer_sequence<int, Ts...>) {
+    uint32_t pa[S::MAXDEG], pb[S::MAXDEG];
     if constexpr (ET) {
-      ((work ? tier<Ts, true>(a, K, r, b0, b1, nm, keep) : void(), __syncthreads()), ...);
+      ((work ? tier<Ts, true>(a, K, r, b0, b1, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb) : void(),
+        __syncthreads()), ...);
     } else {
       (void)work; (void)keep;
-      ((tier<Ts, false>(a, K, r, b0, b1, nm, 0u), __syncthreads()), ...);
+      ((tier<Ts, false>(a, K, r, b0, b1, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb), __syncthreads()), ...);
     }
   }
 
