@@ -35,6 +35,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "decode_io.cuh"
 #include "kernels.h"
 
 namespace qcb {
@@ -481,22 +482,16 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
 
-  // ---- channel LLRs -> [cw][c][j] (coalesced global reads) ------------------
+  // ---- channel LLRs -> [cw][c][j] --------------------------------------------
   {
     const int nthr = blockDim.x;
-    const int dj = nthr / Z, dc = nthr - dj * Z;
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      int j = tid / Z, c = tid - (tid / Z) * Z;
-      if constexpr (A::kElem == 4) {
-        const float* src = reinterpret_cast<const float*>(a.llr) + (cw0 + q) * N;
-        for (int n = tid; n < N; n += nthr) {
-          const float v = A::canon(__ldcs(src + n));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(cb + c * RS + j * 4), "f"(v));
-          c += dc; j += dj;
-          if (c >= Z) { c -= Z; ++j; }
-        }
-      } else {
+    if constexpr (A::kElem == 4) {
+      load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
+    } else {
+      const int dj = nthr / Z, dc = nthr - dj * Z;
+      for (int q = 0; q < ncw; ++q) {
+        const uint32_t cb = sbase + (uint32_t)q * cws;
+        int j = tid / Z, c = tid - (tid / Z) * Z;
         const short* src = reinterpret_cast<const short*>(a.llr) + (cw0 + q) * N;
         for (int n = tid; n < N; n += nthr) {
           const short v = __ldcs(src + n);
@@ -517,31 +512,47 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   for (int e = 0; e < S::NE; ++e) msg[e] = A::zero();
 
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
-  for (int k = 0; k < a.max_iters; ++k) {
-    const bool work = act && !(ET && s_done[g]);
-    L::template sweep<ET>(a, K, rs, b0, b1, msg, work, tiers);
-    const bool last = (k + 1 == a.max_iters);
-    if (ET || last) {                           // syndrome (_kernels.py:85-96)
+  if constexpr (!ET) {
+    // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, msg, act, tiers);
+    if (a.max_iters > 0) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (work && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
+      if (act && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
       __syncthreads();
     }
-    if (tid == 0) s_active = 0;
-    __syncthreads();
-    if (tid < ncw && !s_done[tid]) {
-      s_iters[tid] = k + 1;
-      if (ET && !s_fail[tid]) s_done[tid] = 1;  // converged: frozen from now on
-      else s_active = 1;
+    if (tid < ncw) s_iters[tid] = a.max_iters;
+  } else {
+    for (int k = 0; k < a.max_iters; ++k) {
+      const bool work = act && !s_done[g];
+      L::template sweep<true>(a, K, rs, b0, b1, msg, work, tiers);
+      if (tid < kLayMaxCw) s_fail[tid] = 0;     // syndrome (_kernels.py:85-96)
+      __syncthreads();
+      if (work && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
+      if (tid == 0) s_active = 0;
+      __syncthreads();
+      if (tid < ncw && !s_done[tid]) {
+        s_iters[tid] = k + 1;
+        if (!s_fail[tid]) s_done[tid] = 1;      // converged: frozen from now on
+        else s_active = 1;
+      }
+      __syncthreads();
+      if (!s_active) break;
     }
-    __syncthreads();
-    if (!s_active) break;
   }
 
   // ---- outputs: iterations, converged, hard decisions, posteriors -------------
   if (tid < ncw) {
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
+  }
+  if constexpr (A::kElem == 4) {
+    uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
+    float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
+    store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
+                         [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
+                         [](uint32_t v) { return __uint_as_float(v); });
+    return;
   }
   const int nthr = blockDim.x;
   if (a.hard_packed) {

@@ -191,33 +191,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
-    const int nthr = blockDim.x;
-    const short* llr = reinterpret_cast<const short*>(a.llr);
-    const bool al4 = ((reinterpret_cast<uintptr_t>(llr) | (uintptr_t)(N * 2)) & 3) == 0;
-    for (int q = 0; q < npairs; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      const short* sa = llr + (cw0 + 2 * q) * N;
-      const bool hasb = 2 * q + 1 < ncw;
-      const short* sb = hasb ? sa + N : sa;
-      if (al4) {
-        const uint32_t* ua = reinterpret_cast<const uint32_t*>(sa);
-        const uint32_t* ub = reinterpret_cast<const uint32_t*>(sb);
-        for (int i = tid; i < (N >> 1); i += nthr) {
-          const int n = 2 * i;
-          const int j = n / Z, c = n - j * Z;
-          const uint32_t x = __ldcs(ua + i), y = hasb ? __ldcs(ub + i) : 0u;
-          ArithI16x2::sts(cb + c * RS + j * 4, __byte_perm(x, y, 0x5410));
-          const int c1 = c + 1 == Z ? 0 : c + 1, j1 = c + 1 == Z ? j + 1 : j;
-          ArithI16x2::sts(cb + c1 * RS + j1 * 4, __byte_perm(x, y, 0x7632));
-        }
-      } else {
-        for (int n = tid; n < N; n += nthr) {
-          const int j = n / Z, c = n - j * Z;
-          const uint32_t x = (uint16_t)__ldcs(sa + n), y = hasb ? (uint16_t)__ldcs(sb + n) : 0u;
-          ArithI16x2::sts(cb + c * RS + j * 4, x | (y << 16));
-        }
-      }
-    }
+    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -229,35 +203,43 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   for (int e = 0; e < S::NE; ++e) nm[e] = 0u;
 
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
-  for (int k = 0; k < a.max_iters; ++k) {
-    bool work = act;
-    uint32_t keep = 0;
-    if constexpr (ET) {
-      const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
-      work = act && !(da && db);
-      keep = (da ? 0x0000FFFFu : 0u) | (db ? 0xFFFF0000u : 0u);
-    }
-    L::template sweep<ET>(a, K, rs, b0, b1, nm, work, keep, tiers);
-    const bool last = (k + 1 == a.max_iters);
-    if (ET || last) {                           // syndrome (_kernels.py:85-96)
+  if constexpr (!ET) {
+    // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, nm, act, 0u, tiers);
+    if (a.max_iters > 0) {
       if (tid < MAXC) s_fail[tid] = 0;
       __syncthreads();
-      if (work) {
+      if (act) {
         const uint32_t par = L::parity_all(a, rs, b0, b1, tiers);
         if (par & 1u) s_fail[2 * g] = 1;
         if (par & 2u) s_fail[2 * g + 1] = 1;
       }
       __syncthreads();
     }
-    if (tid == 0) s_active = 0;
-    __syncthreads();
-    if (tid < ncw && !s_done[tid]) {
-      s_iters[tid] = k + 1;
-      if (ET && !s_fail[tid]) s_done[tid] = 1;
-      else s_active = 1;
+    if (tid < ncw) s_iters[tid] = a.max_iters;
+  } else {
+    for (int k = 0; k < a.max_iters; ++k) {
+      const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
+      const bool work = act && !(da && db);
+      const uint32_t keep = (da ? 0x0000FFFFu : 0u) | (db ? 0xFFFF0000u : 0u);
+      L::template sweep<true>(a, K, rs, b0, b1, nm, work, keep, tiers);
+      if (tid < MAXC) s_fail[tid] = 0;          // syndrome (_kernels.py:85-96)
+      __syncthreads();
+      if (work) {
+        const uint32_t par = L::parity_all(a, rs, b0, b1, tiers);
+        if (par & 1u) s_fail[2 * g] = 1;
+        if (par & 2u) s_fail[2 * g + 1] = 1;
+      }
+      if (tid == 0) s_active = 0;
+      __syncthreads();
+      if (tid < ncw && !s_done[tid]) {
+        s_iters[tid] = k + 1;
+        if (!s_fail[tid]) s_done[tid] = 1;
+        else s_active = 1;
+      }
+      __syncthreads();
+      if (!s_active) break;
     }
-    __syncthreads();
-    if (!s_active) break;
   }
 
   // ---- outputs ---------------------------------------------------------------
@@ -265,44 +247,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
-  const int nthr = blockDim.x;
-  auto lane_val = [&](int q, int n) -> int {     // int16 posterior of codeword q (of this CTA), bit n
-    const int j = n / Z, c = n - j * Z;
-    const uint32_t v = ArithI16x2::lds(sbase + (uint32_t)(q >> 1) * cws + c * RS + j * 4);
-    return (q & 1) ? ((int)v >> 16) : sext16((int)v);
-  };
-  if (a.hard_packed) {
-    const int nbytes = (N + 7) >> 3;
-    uint8_t* hp = reinterpret_cast<uint8_t*>(a.hard) + cw0 * nbytes;
-    for (int i = tid; i < ncw * nbytes; i += nthr) {
-      const int q = i / nbytes, b = i - q * nbytes;
-      uint32_t byte = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int n = b * 8 + u;
-        byte = (byte << 1) | ((n < N && lane_val(q, n) <= 0) ? 1u : 0u);
-      }
-      hp[i] = (uint8_t)byte;
-    }
-  } else {
-    uint8_t* h = reinterpret_cast<uint8_t*>(a.hard) + cw0 * N;
-    for (int q = 0; q < ncw; ++q) {
-      for (int n4 = tid * 4; n4 < N; n4 += nthr * 4) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (n4 + u < N && lane_val(q, n4 + u) <= 0) word |= 1u << (8 * u);
-        uint8_t* dst = h + (int64_t)q * N + n4;
-        if (n4 + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) *reinterpret_cast<uint32_t*>(dst) = word;
-        else for (int u = 0; n4 + u < N; ++u) dst[u] = (uint8_t)(word >> (8 * u));
-      }
-    }
-  }
-  if (a.post) {
-    int16_t* po = reinterpret_cast<int16_t*>(a.post);
-    for (int q = 0; q < ncw; ++q)
-      for (int n = tid; n < N; n += nthr) po[(cw0 + q) * N + n] = (int16_t)lane_val(q, n);
-  }
+  store_outputs_pair16(reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N), a.hard_packed,
+                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, Z, sbase, cws, RS);
 }
 
 template <class S, int ZS, bool ET>
