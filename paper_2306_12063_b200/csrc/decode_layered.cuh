@@ -98,6 +98,7 @@ struct RtK {              // runtime constants (kernel parameters)
 struct ArithF32 {
   using Val = float;                     // posterior / message value
   static constexpr int kElem = 4;        // bytes per shared-memory cell
+  static constexpr int kKind = 0;        // address-table policy key (use_addr_tab)
 
   __device__ static Val lds(uint32_t a) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
   __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
@@ -178,6 +179,7 @@ constexpr int kI16LooMaxDeg = QCB_I16_LOO_MAXDEG;
 struct ArithI16 {
   using Val = uint32_t;
   static constexpr int kElem = 2;
+  static constexpr int kKind = 1;
 
   __device__ static Val lds(uint32_t a) {
     short v; asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a)); return (uint32_t)(int)v;
@@ -306,6 +308,139 @@ __device__ __forceinline__ void tier_addrs(const SpecArgs& a, int r, uint32_t b0
   ((addr[Ks] = edge_addr<S, A, ZS, E0 + Ks>(a, r, b0, b1)), ...);
 }
 
+// Per-thread shared-memory address table.  Every edge whose circulant shift
+// is not a compile-time zero needs `(r >= Z - e) ? b1 : b0` (ISETP + SEL on
+// the half-rate ALU pipe: 21 % of the float32 kernel's ALU instructions on
+// C2, measured); the addresses are the same in every sweep, so each thread
+// computes them once and keeps them in shared memory, and a tier fetches its
+// addresses with one LDS.64 per two edges (the LSU pipe has the headroom).
+// Layout [thread][unit], unit = 2 addresses, an odd number of units per
+// thread so that a half-warp's LDS.64 hits 16 distinct bank pairs.
+#ifndef QCB_ADDR_TAB
+#define QCB_ADDR_TAB 1
+#endif
+// Measured per structure (tools/exp/percode.py, round 1, table vs selects):
+// float32 gains on WiMAX 2/3B, 3/4A, 3/4B (+7..11 %) and loses on every Wi-Fi
+// code and WiMAX 1/2 (-6..-22 %: those keep enough addresses hoisted in
+// registers); the int16 pair kernel gains on all WiMAX codes (+5..24 %) and
+// Wi-Fi 1944 R2/3, R3/4 (+16 %), loses on Wi-Fi 648 R3/4, R5/6 and 1296 R5/6.
+template <class S, class A>
+constexpr bool use_addr_tab() {
+  constexpr unsigned kF32 = (1u << 14) | (1u << 15) | (1u << 16);
+  constexpr unsigned kPair16 = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 6) | (1u << 8) | (1u << 9) |
+                               (0x3Fu << 12);
+  return QCB_ADDR_TAB && ((A::kKind == 0 && ((kF32 >> S::ID) & 1u)) || (A::kKind == 2 && ((kPair16 >> S::ID) & 1u)));
+}
+
+template <class S, int ZS, bool TAB>
+struct AddrTab {
+  static constexpr bool in_tab(int e) { return TAB && (ZS == 0 || S::SHIFT0[e] != 0); }
+  static constexpr int tier_of(int e) {
+    int t = 0;
+    while (S::START[t + 1] <= e) ++t;
+    return t;
+  }
+  static constexpr int count(int t) {
+    int c = 0;
+    for (int e = S::START[t]; e < S::START[t + 1]; ++e) c += in_tab(e) ? 1 : 0;
+    return c;
+  }
+  static constexpr int unit0(int t) {
+    int u = 0;
+    for (int i = 0; i < t; ++i) u += (count(i) + 1) / 2;
+    return u;
+  }
+  static constexpr int units() {
+    const int u = unit0(S::MB);
+    return u == 0 ? 0 : (u | 1);
+  }
+  static constexpr int entry(int e) {           // index in the thread's flat table
+    const int t = tier_of(e);
+    int c = 0;
+    for (int x = S::START[t]; x < e; ++x) c += in_tab(x) ? 1 : 0;
+    return 2 * unit0(t) + c;
+  }
+};
+
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+
+template <class S, class A, int ZS, bool TAB, int E>
+__device__ __forceinline__ uint32_t tab_pick(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, const uint32_t* ent,
+                                             int base) {
+  if constexpr (AddrTab<S, ZS, TAB>::in_tab(E)) return ent[AddrTab<S, ZS, TAB>::entry(E) - base];
+  else return edge_addr<S, A, ZS, E>(a, r, b0, b1);
+}
+
+// addresses of tier T's edges: table entries + the compile-time zero-shift ones
+template <class S, class A, int ZS, bool TAB, int E0, int... Ks>
+__device__ __forceinline__ void tier_addrs_tab(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab,
+                                               uint32_t* addr, std::integer_sequence<int, Ks...>) {
+  using AT = AddrTab<S, ZS, TAB>;
+  constexpr int T = AT::tier_of(E0);
+  constexpr int NU = (AT::count(T) + 1) / 2;
+  uint32_t ent[2 * NU + 2];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    const uint2 v = lds64(tab + (uint32_t)((AT::unit0(T) + u) * 8));
+    ent[2 * u] = v.x;
+    ent[2 * u + 1] = v.y;
+  }
+  ((addr[Ks] = tab_pick<S, A, ZS, TAB, E0 + Ks>(a, r, b0, b1, ent, 2 * AT::unit0(T))), ...);
+}
+
+// split form: fetch tier T's table entries (issued a tier ahead), then compose
+template <class S, int ZS, bool TAB>
+constexpr int tab_max_entries() {
+  int m = 2;
+  for (int t = 0; t < S::MB; ++t) {
+    const int e = 2 * ((AddrTab<S, ZS, TAB>::count(t) + 1) / 2);
+    if (e > m) m = e;
+  }
+  return m;
+}
+template <class S, int ZS, bool TAB, int T>
+__device__ __forceinline__ void tab_fetch(uint32_t tab, uint32_t* ent) {
+  using AT = AddrTab<S, ZS, TAB>;
+  if constexpr (T < S::MB) {
+    constexpr int NU = (AT::count(T) + 1) / 2;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      const uint2 v = lds64(tab + (uint32_t)((AT::unit0(T) + u) * 8));
+      ent[2 * u] = v.x;
+      ent[2 * u + 1] = v.y;
+    }
+  }
+}
+template <class S, class A, int ZS, bool TAB, int T, int... Ks>
+__device__ __forceinline__ void tab_compose(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, const uint32_t* ent,
+                                            uint32_t* addr, std::integer_sequence<int, Ks...>) {
+  ((addr[Ks] = tab_pick<S, A, ZS, TAB, S::START[T] + Ks>(a, r, b0, b1, ent, 2 * AddrTab<S, ZS, TAB>::unit0(T))), ...);
+}
+
+template <class S, class A, int ZS, bool TAB, int... Es>
+__device__ __forceinline__ void fill_addr_tab(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab,
+                                              std::integer_sequence<int, Es...>) {
+  using AT = AddrTab<S, ZS, TAB>;
+  constexpr int NU = AT::units();
+  if constexpr (NU > 0) {
+    uint32_t ent[2 * NU];
+#pragma unroll
+    for (int i = 0; i < 2 * NU; ++i) ent[i] = 0u;
+    ((AT::in_tab(Es) ? (void)(ent[AT::entry(Es)] = edge_addr<S, A, ZS, Es>(a, r, b0, b1)) : void()), ...);
+#pragma unroll
+    for (int u = 0; u < NU; ++u) sts64(tab + (uint32_t)(u * 8), ent[2 * u], ent[2 * u + 1]);
+  }
+}
+template <class S, int ZS, bool TAB>
+constexpr int addr_tab_bytes_per_thread() { return AddrTab<S, ZS, TAB>::units() * 8; }
+
 // Edge k of tier T reads a block column that tier T-1 does not write: its
 // posterior is final once tier T-2's barrier has passed, so it can be loaded
 // before tier T-1's barrier (a tier writes exactly its own block
@@ -335,42 +470,43 @@ template <class S, class A, int ZS>
 struct Layered {
   using Val = typename A::Val;
 
-  // early loads of tier T (issued at the end of tier T-1, before its barrier)
-  template <int T>
-  __device__ __forceinline__ static void load_early(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
-                                                    Val (&pe)[S::MAXDEG]) {
-    if constexpr (T < S::MB) {
-      constexpr int D = S::DEG[T];
-      uint32_t addr[D];
-      tier_addrs<S, A, ZS, S::START[T]>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
-#pragma unroll
-      for (int k = 0; k < D; ++k)
-        if (early_edge<S, T>(k)) pe[k] = A::lds(addr[k]);
-    }
-  }
+  static constexpr bool TAB = use_addr_tab<S, A>();
+  static constexpr int ME = tab_max_entries<S, ZS, TAB>();
 
+  // tier T: its table entries arrived in ec (fetched during tier T-1); fetch
+  // tier T+1's into en, load the late posteriors, update, store, then load
+  // tier T+1's early posteriors (early_edge) before the barrier
   template <int T>
   __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                              Val (&msg)[S::NE], Val (&pe)[S::MAXDEG], Val (&pn)[S::MAXDEG]) {
+                                              uint32_t tab, Val (&msg)[S::NE], Val (&pe)[S::MAXDEG],
+                                              Val (&pn)[S::MAXDEG], uint32_t (&ec)[ME], uint32_t (&en)[ME]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
     Val p[D], o[D];
-    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ec, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
+    tab_fetch<S, ZS, TAB, T + 1>(tab, en);
     A::template row<D>(p, o, msg + E0, K);
 #pragma unroll
     for (int k = 0; k < D; ++k) A::sts(addr[k], o[k]);
-    load_early<T + 1>(a, r, b0, b1, pn);
+    if constexpr (T + 1 < S::MB && EarlyMask<S, T + 1>::value != 0) {
+      constexpr int DN = S::DEG[T + 1];
+      uint32_t an[DN];
+      tab_compose<S, A, ZS, TAB, T + 1>(a, r, b0, b1, en, an, std::make_integer_sequence<int, DN>{});
+#pragma unroll
+      for (int k = 0; k < DN; ++k)
+        if (early_edge<S, T + 1>(k)) pn[k] = A::lds(an[k]);
+    }
   }
 
   template <int T>
-  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
-    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    tier_addrs_tab<S, A, ZS, TAB, E0>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
     uint32_t par = 0;
 #pragma unroll
     for (int k = 0; k < D; ++k) par ^= A::hard(A::lds(addr[k])) ? 1u : 0u;
@@ -381,21 +517,28 @@ struct Layered {
   // the batch work on scratch / unused slots): no branch around the tier body
   template <bool ET, int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                               Val (&msg)[S::NE], bool work, std::integer_sequence<int, Ts...>) {
+                                               uint32_t tab, Val (&msg)[S::NE], bool work,
+                                               std::integer_sequence<int, Ts...>) {
     Val pa[S::MAXDEG], pb[S::MAXDEG];
+    uint32_t ea[ME], eb[ME];
+    tab_fetch<S, ZS, TAB, 0>(tab, ea);
     if constexpr (ET) {
-      ((work ? tier<Ts>(a, K, r, b0, b1, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb) : void(),
+      ((work ? tier<Ts>(a, K, r, b0, b1, tab, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
+                        (Ts & 1) ? ea : eb)
+             : void(),
         __syncthreads()), ...);
     } else {
       (void)work;
-      ((tier<Ts>(a, K, r, b0, b1, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb), __syncthreads()), ...);
+      ((tier<Ts>(a, K, r, b0, b1, tab, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
+                 (Ts & 1) ? ea : eb),
+        __syncthreads()), ...);
     }
   }
 
   template <int... Ts>
   __device__ __forceinline__ static uint32_t parity_all(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
-                                                        std::integer_sequence<int, Ts...>) {
-    return (parity<Ts>(a, r, b0, b1) | ...);
+                                                        uint32_t tab, std::integer_sequence<int, Ts...>) {
+    return (parity<Ts>(a, r, b0, b1, tab) | ...);
   }
 };
 
@@ -481,6 +624,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+  // this thread's address table (after the G + 1 posterior blocks)
+  // the scratch block G exists only when the last warp has padding threads
+  const uint32_t nblk = (int)blockDim.x > G * Z ? (uint32_t)G + 1 : (uint32_t)G;
+  const uint32_t tab = sbase + nblk * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  fill_addr_tab<S, A, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
 
   // ---- channel LLRs -> [cw][c][j] --------------------------------------------
   {
@@ -514,21 +662,21 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   if constexpr (!ET) {
     // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
-    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, msg, act, tiers);
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, msg, act, tiers);
     if (a.max_iters > 0) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (act && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
+      if (act && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[g] = 1;
       __syncthreads();
     }
     if (tid < ncw) s_iters[tid] = a.max_iters;
   } else {
     for (int k = 0; k < a.max_iters; ++k) {
       const bool work = act && !s_done[g];
-      L::template sweep<true>(a, K, rs, b0, b1, msg, work, tiers);
+      L::template sweep<true>(a, K, rs, b0, b1, tab, msg, work, tiers);
       if (tid < kLayMaxCw) s_fail[tid] = 0;     // syndrome (_kernels.py:85-96)
       __syncthreads();
-      if (work && L::parity_all(a, rs, b0, b1, tiers)) s_fail[g] = 1;
+      if (work && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[g] = 1;
       if (tid == 0) s_active = 0;
       __syncthreads();
       if (tid < ncw && !s_done[tid]) {
@@ -618,9 +766,10 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
 }
 
 template <class K>
-inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s) {
+inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)(a.pairs + 1) * ((z * rs + 15) & ~15);
+  const int nblk = threads > a.pairs * z ? a.pairs + 1 : a.pairs;   // + scratch block for padding threads
+  const size_t smem = (size_t)nblk * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
@@ -643,7 +792,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
-  return launch_layered_fixed(kern, b, z, RS, s);
+  return launch_layered_fixed(kern, b, z, RS, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>());
 }
 
 }  // namespace qcb

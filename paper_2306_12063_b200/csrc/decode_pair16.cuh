@@ -46,6 +46,7 @@ __device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
 struct ArithI16x2 {
   using Val = uint32_t;
   static constexpr int kElem = 4;        // one cell = the two codewords' int16 posteriors
+  static constexpr int kKind = 2;        // address-table policy key (use_addr_tab)
 
   __device__ static Val lds(uint32_t a) { uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
   __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
@@ -86,18 +87,24 @@ template <class S, int ZS>
 struct Layered2 {
   using A = ArithI16x2;
 
+  static constexpr bool TAB = use_addr_tab<S, A>();
+  static constexpr int ME = tab_max_entries<S, ZS, TAB>();
+
   // keep: lanes of converged codewords (early termination) keep their posteriors;
-  // pe: this tier's early-loaded posteriors, pn: next tier's (early_edge)
+  // pe / pn: this / the next tier's early-loaded posteriors (early_edge);
+  // ec / en: this / the next tier's address-table entries
   template <int T, bool ET>
   __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                              uint32_t (&nm)[S::NE], uint32_t keep, uint32_t (&pe)[S::MAXDEG],
-                                              uint32_t (&pn)[S::MAXDEG]) {
+                                              uint32_t tab, uint32_t (&nm)[S::NE], uint32_t keep,
+                                              uint32_t (&pe)[S::MAXDEG], uint32_t (&pn)[S::MAXDEG],
+                                              uint32_t (&ec)[ME], uint32_t (&en)[ME]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D], p[D], o[D];
-    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ec, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
+    tab_fetch<S, ZS, TAB, T + 1>(tab, en);
     A::template row<D>(p, o, nm + E0, K);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -105,10 +112,10 @@ struct Layered2 {
       if constexpr (ET) v = (v & ~keep) | (p[k] & keep);       // converged lanes keep their posteriors
       A::sts(addr[k], v);
     }
-    if constexpr (T + 1 < S::MB) {
+    if constexpr (T + 1 < S::MB && EarlyMask<S, T + 1>::value != 0) {
       constexpr int DN = S::DEG[T + 1];
       uint32_t an[DN];
-      tier_addrs<S, A, ZS, S::START[T + 1]>(a, r, b0, b1, an, std::make_integer_sequence<int, DN>{});
+      tab_compose<S, A, ZS, TAB, T + 1>(a, r, b0, b1, en, an, std::make_integer_sequence<int, DN>{});
 #pragma unroll
       for (int k = 0; k < DN; ++k)
         if (early_edge<S, T + 1>(k)) pn[k] = A::lds(an[k]);
@@ -116,11 +123,11 @@ struct Layered2 {
   }
 
   template <int T>
-  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
-    tier_addrs<S, A, ZS, E0>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    tier_addrs_tab<S, A, ZS, TAB, E0>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
     uint32_t par = 0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -133,22 +140,28 @@ struct Layered2 {
 
   template <bool ET, int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                               uint32_t (&nm)[S::NE], bool work, uint32_t keep,
+                                               uint32_t tab, uint32_t (&nm)[S::NE], bool work, uint32_t keep,
                                                std::integer_sequence<int, Ts...>) {
     uint32_t pa[S::MAXDEG], pb[S::MAXDEG];
+    uint32_t ea[ME], eb[ME];
+    tab_fetch<S, ZS, TAB, 0>(tab, ea);
     if constexpr (ET) {
-      ((work ? tier<Ts, true>(a, K, r, b0, b1, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb) : void(),
+      ((work ? tier<Ts, true>(a, K, r, b0, b1, tab, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
+                              (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
+             : void(),
         __syncthreads()), ...);
     } else {
       (void)work; (void)keep;
-      ((tier<Ts, false>(a, K, r, b0, b1, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb), __syncthreads()), ...);
+      ((tier<Ts, false>(a, K, r, b0, b1, tab, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
+                        (Ts & 1) ? ea : eb),
+        __syncthreads()), ...);
     }
   }
 
   template <int... Ts>
   __device__ __forceinline__ static uint32_t parity_all(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
-                                                        std::integer_sequence<int, Ts...>) {
-    return (parity<Ts>(a, r, b0, b1) | ...);
+                                                        uint32_t tab, std::integer_sequence<int, Ts...>) {
+    return (parity<Ts>(a, r, b0, b1, tab) | ...);
   }
 };
 
@@ -188,6 +201,10 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+  // the scratch block G exists only when the last warp has padding threads
+  const uint32_t nblk = (int)blockDim.x > G * Z ? (uint32_t)G + 1 : (uint32_t)G;
+  const uint32_t tab = sbase + nblk * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  fill_addr_tab<S, ArithI16x2, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
@@ -205,12 +222,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   if constexpr (!ET) {
     // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
-    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, nm, act, 0u, tiers);
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
     if (a.max_iters > 0) {
       if (tid < MAXC) s_fail[tid] = 0;
       __syncthreads();
       if (act) {
-        const uint32_t par = L::parity_all(a, rs, b0, b1, tiers);
+        const uint32_t par = L::parity_all(a, rs, b0, b1, tab, tiers);
         if (par & 1u) s_fail[2 * g] = 1;
         if (par & 2u) s_fail[2 * g + 1] = 1;
       }
@@ -222,11 +239,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
       const bool work = act && !(da && db);
       const uint32_t keep = (da ? 0x0000FFFFu : 0u) | (db ? 0xFFFF0000u : 0u);
-      L::template sweep<true>(a, K, rs, b0, b1, nm, work, keep, tiers);
+      L::template sweep<true>(a, K, rs, b0, b1, tab, nm, work, keep, tiers);
       if (tid < MAXC) s_fail[tid] = 0;          // syndrome (_kernels.py:85-96)
       __syncthreads();
       if (work) {
-        const uint32_t par = L::parity_all(a, rs, b0, b1, tiers);
+        const uint32_t par = L::parity_all(a, rs, b0, b1, tab, tiers);
         if (par & 1u) s_fail[2 * g] = 1;
         if (par & 2u) s_fail[2 * g + 1] = 1;
       }
@@ -264,7 +281,8 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)(b.pairs + 1) * ((z * RS + 15) & ~15);   // + scratch slot
+  const int nblk = thr > b.pairs * z ? b.pairs + 1 : b.pairs;        // + scratch block for padding threads
+  const size_t smem = (size_t)nblk * ((z * RS + 15) & ~15) + (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t per = 2 * (int64_t)b.pairs;

@@ -137,6 +137,22 @@ struct LayeredTm {
     if constexpr (A::kElem == 4) return __float_as_uint(v); else return v;
   }
 
+  template <int T>
+  __device__ __forceinline__ static uint32_t parity(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
+    constexpr int D = S::DEG[T];
+    uint32_t addr[D];
+    tier_addrs<S, A, ZS, S::START[T]>(a, r, b0, b1, addr, std::make_integer_sequence<int, D>{});
+    uint32_t par = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) par ^= A::hard(A::lds(addr[k])) ? 1u : 0u;
+    return par;
+  }
+  template <int... Ts>
+  __device__ __forceinline__ static uint32_t parity_all(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                        std::integer_sequence<int, Ts...>) {
+    return (parity<Ts>(a, r, b0, b1) | ...);
+  }
+
   template <int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
                                                uint32_t tb, uint32_t (&bufA)[S::MAXDEG],
@@ -247,7 +263,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
     if (ET || last) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (work && L::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
+      if (work && LT::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
       __syncthreads();
     }
     if (tid == 0) s_active = 0;
