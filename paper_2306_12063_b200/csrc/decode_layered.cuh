@@ -136,15 +136,24 @@ struct ArithF32 {
     if (D & 1) sx ^= __float_as_uint(zz[D - 1]);
     const uint32_t sxm = sx & 0x80000000u;
     // leave-one-out minima of |zz|
+    // chains step two edges at a time through 3-input mins (FMNMX3), odd
+    // entries hang off them: depth ~D/2 instead of D, same instruction count
     float pre[D], suf[D], ex[D];
     pre[1] = fabsf(zz[0]);
 #pragma unroll
-    for (int k = 2; k < D; ++k) pre[k] = k == 2 ? fminf(fminf(fabsf(zz[0]), fabsf(zz[1])), f_inf())
-                                               : fminf(pre[k - 1], fabsf(zz[k - 1]));
+    for (int k = 2; k < D; ++k) {
+      if (k == 2) pre[2] = fminf(fminf(fabsf(zz[0]), fabsf(zz[1])), f_inf());
+      else if (k & 1) pre[k] = fminf(pre[k - 1], fabsf(zz[k - 1]));
+      else pre[k] = fminf(fminf(pre[k - 2], fabsf(zz[k - 2])), fabsf(zz[k - 1]));
+    }
     suf[D - 2] = fabsf(zz[D - 1]);
 #pragma unroll
-    for (int k = D - 3; k >= 0; --k) suf[k] = k == D - 3 ? fminf(fminf(fabsf(zz[D - 1]), fabsf(zz[D - 2])), f_inf())
-                                                          : fminf(suf[k + 1], fabsf(zz[k + 1]));
+    for (int k = D - 3; k >= 0; --k) {
+      const int m = D - 1 - k;                  // number of |zz| folded into suf[k]
+      if (k == D - 3) suf[k] = fminf(fminf(fabsf(zz[D - 1]), fabsf(zz[D - 2])), f_inf());
+      else if (m & 1) suf[k] = fminf(suf[k + 1], fabsf(zz[k + 1]));
+      else suf[k] = fminf(fminf(suf[k + 2], fabsf(zz[k + 2])), fabsf(zz[k + 1]));
+    }
     ex[0] = D == 2 ? fminf(suf[0], f_inf()) : suf[0];
     ex[D - 1] = D == 2 ? fminf(pre[D - 1], f_inf()) : pre[D - 1];
 #pragma unroll

@@ -66,15 +66,24 @@ struct ArithI16x2 {
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
     if (D & 1) sx ^= d[D - 1];
-    uint32_t suf[D];
+    // suffix / prefix chains step two edges at a time (VIMNMX3.S16x2)
+    uint32_t suf[D], pre[D];
     suf[D - 2] = a[D - 1];
 #pragma unroll
-    for (int k = D - 3; k >= 0; --k) suf[k] = vmin2(suf[k + 1], a[k + 1]);
-    uint32_t pre = a[0];
+    for (int k = D - 3; k >= 0; --k) {
+      const int m = D - 1 - k;
+      if (k == D - 3 || (m & 1)) suf[k] = vmin2(suf[k + 1], a[k + 1]);
+      else suf[k] = vmin2(vmin2(suf[k + 2], a[k + 2]), a[k + 1]);
+    }
+    pre[1] = a[0];
+#pragma unroll
+    for (int k = 2; k < D; ++k) {
+      if (k == 2 || (k & 1)) pre[k] = vmin2(pre[k - 1], a[k - 1]);
+      else pre[k] = vmin2(vmin2(pre[k - 2], a[k - 2]), a[k - 1]);
+    }
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const uint32_t ex = k == 0 ? suf[0] : (k == D - 1 ? pre : vmin2(pre, suf[k]));
-      if (k > 0 && k < D - 1) pre = vmin2(pre, a[k]);
+      const uint32_t ex = k == 0 ? suf[0] : (k == D - 1 ? pre[D - 1] : vmin2(pre[k], suf[k]));
       const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
       const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
       o[k] = vadd2(d[k], (nex & m) | (ex & ~m));                   // post = zz + L_new

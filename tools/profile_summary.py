@@ -2,6 +2,7 @@
 
     python tools/profile_summary.py gpurun_out/prof_c2.ncu-rep C2 profiles/r01_ncu_summary.json
     python tools/profile_summary.py --launches gpurun_out/launches_c2.csv C2 profiles/r01_launches_c2.json
+    python tools/profile_summary.py --phases gpurun_out/prof_c2.ncu-rep C2 profiles/r01_ncu_summary.json
 
 For a `--set full` report: per-launch duration, DRAM bytes (the `traffic`
 figure bench.py reports), issue utilisation, pipe utilisation, occupancy,
@@ -81,6 +82,31 @@ def full(rep: str, config: str, out: str) -> None:
     print(json.dumps(data[config], indent=1))
 
 
+def phases(rep: str, config: str, out: str) -> None:
+    """Warp-sample share of the code between consecutive barriers (SASS
+    source view): prologue (LLR load), the tier segments, syndrome /
+    bookkeeping, epilogue (outputs)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, data = rows[1], rows[2:]
+    i_src, i_all = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
+    i_ex = hdr.index("Instructions Executed")
+    tot = sum(int(r[i_all]) for r in data if r[i_all].isdigit()) or 1
+    segs, cum, last = [], 0, 0
+    for r in data:
+        cum += int(r[i_all]) if r[i_all].isdigit() else 0
+        if "BAR.SYNC" in r[i_src] or "EXIT" in r[i_src]:
+            segs.append({"ends_at": r[i_src].strip()[:24], "executed": _num(r[i_ex]),
+                         "sample_pct": round(100 * (cum - last) / tot, 1)})
+            last = cum
+    p = Path(out)
+    data_out = json.loads(p.read_text()) if p.exists() else {}
+    data_out[config + "_phases"] = {"source": Path(rep).name, "segments": segs}
+    p.write_text(json.dumps(data_out, indent=1) + "\n")
+    print(json.dumps(segs, indent=1))
+
+
 def launches(csvfile: str, config: str, out: str) -> None:
     text = Path(csvfile).read_text()
     start = text.find('"ID"')
@@ -110,5 +136,7 @@ def launches(csvfile: str, config: str, out: str) -> None:
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(*sys.argv[2:5])
+    elif sys.argv[1] == "--phases":
+        phases(*sys.argv[2:5])
     else:
         full(*sys.argv[1:4])
