@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
     ap.add_argument("--no-encode", action="store_true", help="C5: skip the packed-encoder measurement")
     return ap.parse_args()
