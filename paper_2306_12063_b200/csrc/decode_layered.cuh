@@ -624,19 +624,23 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int g = tid / Z, r = tid - g * Z;
   const int64_t cw0 = (int64_t)blockIdx.x * G;
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
-  const bool act = g < ncw;
   const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);   // bytes per codeword block
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  // padding threads of the last warp (g >= G) use the scratch slot G
-  const int gs = g < G ? g : G, rs = g < G ? r : (tid - G * Z) % Z;
+  // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
+  // warp: same row, same inputs, same instruction stream, so in lockstep they
+  // load and store the very words their twins do (same-word accesses: no bank
+  // conflict, identical values).  A separate scratch block costs a 2-way bank
+  // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
+  // shared-memory wavefronts).
+  const int twin = tid < G * Z ? tid : (tid & ~31) + ((tid & 31) % (G * Z - (tid & ~31)));
+  const int gs = twin / Z, rs = twin - gs * Z;
+  const bool act = gs < ncw;
   // opaque copies keep the row bases in registers (no per-tier rematerialisation)
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
-  // this thread's address table (after the G + 1 posterior blocks)
-  // the scratch block G exists only when the last warp has padding threads
-  const uint32_t nblk = (int)blockDim.x > G * Z ? (uint32_t)G + 1 : (uint32_t)G;
-  const uint32_t tab = sbase + nblk * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  // this thread's address table (after the G posterior blocks)
+  const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
   fill_addr_tab<S, A, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
 
   // ---- channel LLRs -> [cw][c][j] --------------------------------------------
@@ -675,17 +679,17 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
     if (a.max_iters > 0) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (act && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[g] = 1;
+      if (act && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[gs] = 1;
       __syncthreads();
     }
     if (tid < ncw) s_iters[tid] = a.max_iters;
   } else {
     for (int k = 0; k < a.max_iters; ++k) {
-      const bool work = act && !s_done[g];
+      const bool work = act && !s_done[gs];
       L::template sweep<true>(a, K, rs, b0, b1, tab, msg, work, tiers);
       if (tid < kLayMaxCw) s_fail[tid] = 0;     // syndrome (_kernels.py:85-96)
       __syncthreads();
-      if (work && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[g] = 1;
+      if (work && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[gs] = 1;
       if (tid == 0) s_active = 0;
       __syncthreads();
       if (tid < ncw && !s_done[tid]) {
@@ -777,8 +781,7 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
 template <class K>
 inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const int nblk = threads > a.pairs * z ? a.pairs + 1 : a.pairs;   // + scratch block for padding threads
-  const size_t smem = (size_t)nblk * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes;
+  const size_t smem = (size_t)a.pairs * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;

@@ -203,16 +203,21 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const int64_t cw0 = (int64_t)blockIdx.x * (2 * G);
   const int ncw = (int)(a.w - cw0 < (int64_t)(2 * G) ? a.w - cw0 : (int64_t)(2 * G));
   const int npairs = (ncw + 1) >> 1;
-  const bool act = g < npairs;
   const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const int gs = g < G ? g : G, rs = g < G ? r : (tid - G * Z) % Z;
+  // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
+  // warp: same row, same inputs, same instruction stream, so in lockstep they
+  // load and store the very words their twins do (same-word accesses: no bank
+  // conflict, identical values).  A separate scratch block costs a 2-way bank
+  // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
+  // shared-memory wavefronts).
+  const int twin = tid < G * Z ? tid : (tid & ~31) + ((tid & 31) % (G * Z - (tid & ~31)));
+  const int gs = twin / Z, rs = twin - gs * Z;
+  const bool act = gs < npairs;
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
-  // the scratch block G exists only when the last warp has padding threads
-  const uint32_t nblk = (int)blockDim.x > G * Z ? (uint32_t)G + 1 : (uint32_t)G;
-  const uint32_t tab = sbase + nblk * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
   fill_addr_tab<S, ArithI16x2, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
@@ -237,8 +242,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       __syncthreads();
       if (act) {
         const uint32_t par = L::parity_all(a, rs, b0, b1, tab, tiers);
-        if (par & 1u) s_fail[2 * g] = 1;
-        if (par & 2u) s_fail[2 * g + 1] = 1;
+        if (par & 1u) s_fail[2 * gs] = 1;
+        if (par & 2u) s_fail[2 * gs + 1] = 1;
       }
       __syncthreads();
     }
@@ -253,8 +258,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       __syncthreads();
       if (work) {
         const uint32_t par = L::parity_all(a, rs, b0, b1, tab, tiers);
-        if (par & 1u) s_fail[2 * g] = 1;
-        if (par & 2u) s_fail[2 * g + 1] = 1;
+        if (par & 1u) s_fail[2 * gs] = 1;
+        if (par & 2u) s_fail[2 * gs + 1] = 1;
       }
       if (tid == 0) s_active = 0;
       __syncthreads();
@@ -290,8 +295,8 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const int nblk = thr > b.pairs * z ? b.pairs + 1 : b.pairs;        // + scratch block for padding threads
-  const size_t smem = (size_t)nblk * ((z * RS + 15) & ~15) + (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
+  const size_t smem = (size_t)b.pairs * ((z * RS + 15) & ~15) +
+                      (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t per = 2 * (int64_t)b.pairs;
