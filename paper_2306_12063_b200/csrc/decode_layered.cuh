@@ -37,6 +37,7 @@
 #include "common.cuh"
 #include "decode_io.cuh"
 #include "kernels.h"
+#include "launch_cache.h"
 
 namespace qcb {
 
@@ -767,13 +768,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 
 // codewords per CTA for a kernel with `regs` registers per thread
 inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
-  if (const char* env = getenv("QCB_CW_PER_CTA")) {   // tuning knob (benchmarks only)
-    const int v = atoi(env);
-    if (v >= 1 && v <= kLayMaxCw && v * z <= kLayMaxThreads) return v;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const int env_v = [] {                        // tuning knob (benchmarks only)
+    const char* env = getenv("QCB_CW_PER_CTA");
+    return env ? atoi(env) : 0;
+  }();
+  if (env_v >= 1 && env_v <= kLayMaxCw && env_v * z <= kLayMaxThreads) return env_v;
+  const int sms = device_sm_count();
   const int cw_smem = (z * kRowStrideUnits * cell_bytes + 15) & ~15;
   return plan_cw_per_cta(z, regs, cw_smem, (double)w / sms);
 }
@@ -782,7 +782,7 @@ template <class K>
 inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
   const size_t smem = (size_t)a.pairs * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
   if (blocks <= 0) return cudaSuccess;
@@ -798,7 +798,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   // the CTA shape is planned from the register count ptxas actually gave
   // this kernel (the decode result does not depend on the CTA size)
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  cudaError_t e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
   b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);

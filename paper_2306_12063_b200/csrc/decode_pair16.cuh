@@ -288,7 +288,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   const int z = ZS > 0 ? ZS : a.z;
   auto kern = decode_pair16_kernel<S, ZS, ET>;
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  cudaError_t e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
   b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4);
@@ -297,7 +297,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   const int thr = (b.pairs * z + 31) / 32 * 32;
   const size_t smem = (size_t)b.pairs * ((z * RS + 15) & ~15) +
                       (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const int64_t per = 2 * (int64_t)b.pairs;
   const int64_t blocks = (a.w + per - 1) / per;

@@ -52,8 +52,11 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   *pair16 = 0;
 
   if (elem == 2) {                          // int16: two codewords per thread in 16x2 lanes
-    const char* p = getenv("QCB_I16_PAIR");
-    if (!(p && p[0] == '0')) {
+    static const bool pair_off = [] {
+      const char* p = getenv("QCB_I16_PAIR");
+      return p && p[0] == '0';
+    }();
+    if (!pair_off) {
       *pair16 = 1;
       *cw_per_cta = 1;                      // planned at launch from the kernel's registers
       *tmem_cols = 0;
@@ -67,8 +70,11 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   const int reg_g = layered_cw_per_cta(z, w, regs_reg, elem);
   *cw_per_cta = reg_g;
   *tmem_cols = 0;
-  const char* env = getenv("QCB_TMEM");
-  if (env && env[0] == '0') return;
+  static const int tmem_env = [] {
+    const char* e = getenv("QCB_TMEM");
+    return e ? (e[0] == '0' ? 0 : (e[0] == '1' ? 1 : -1)) : -1;
+  }();
+  if (tmem_env == 0) return;
   const int regs_tm = QCB_TM_REG_BASE + (elem == 2 ? 6 : 5) * maxdeg;
   const int smem_cw = (z * kRowStrideUnits * elem + 15) & ~15;
   int cols = 0;
@@ -80,7 +86,7 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   // Wi-Fi 1296 R5/6 43.8 / 33.5) and so do the low-degree codes (5-6 %):
   // TMEM reads (64 B/clk/SM) only pay where the register kernel is starved
   const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20;
-  if ((env && env[0] == '1') || prefer) {
+  if (tmem_env == 1 || prefer) {
     *cw_per_cta = g;
     *tmem_cols = cols;
   }

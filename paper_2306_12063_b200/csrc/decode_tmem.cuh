@@ -372,13 +372,13 @@ inline cudaError_t launch_tmem(const SpecArgs& a, cudaStream_t s) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
   const size_t smem = (size_t)a.pairs * ((z * RS + 15) & ~15);
   auto kern = decode_tmem_kernel<S, A, ZS, ET>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   // the register count is only known after ptxas: shrink the CTA if this
   // kernel cannot launch the planned one (the decode result does not depend
   // on the CTA size)
   cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, kern);
+  e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   if (threads > fa.maxThreadsPerBlock) {
     SpecArgs b = a;
