@@ -354,7 +354,7 @@ def run_ours(args, wl):
     alu_peak = sms * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     # the int16 kernel carries two codewords per 32-bit lane (16x2 SIMD):
     # its peak counts 2x so the fraction stays <= 1
-    simd = 2 if (wl.fixed and os.environ.get("QCB_I16_PAIR", "1") != "0") else 1
+    simd = 2 if wl.fixed else 1
     alu_peak *= simd
     kavg = statistics.mean(kernel_ms) * 1e-3
     achieved = edge_updates(wl) * OPS_PER_EDGE_UPDATE / kavg / 1e12

@@ -1,34 +1,41 @@
-// decode_layered.cuh -- layered single-scan min-sum on sm_100a for the 18
-// standard base-matrix structures, float32 and wrap-around int16.
+// decode_layered.cuh -- float32 layered single-scan min-sum on sm_100a for
+// the 18 standard base-matrix structures (the int16 kernel, two codewords per
+// thread in 16x2 lanes, is decode_pair16.cuh and reuses the addressing,
+// address tables and early loads defined here).
 //
-// Reference: /root/reference/pkg/src/qcldpc/_kernels.py:17-100 (float32) and
-// :103-186 (int16).  Bit-exact: every value the reference computes
-// (zz = post - L_old, |zz|, min1/min2, L_new, post = zz + L_new,
-// hard = post <= 0, the syndrome) is produced by the same float32 / int16
-// operation on the same operands; only the way selections are made differs.
+// Reference: /root/reference/pkg/src/qcldpc/_kernels.py:17-100.  Bit-exact:
+// every value the reference computes (zz = post - L_old, |zz|, min1/min2,
+// L_new, post = zz + L_new, hard = post <= 0, the syndrome) is produced by the
+// same float32 operation on the same operands; only the way selections are
+// made differs.
 //
 // Mapping (why, with the ncu evidence):
 //  * one thread = one check row r of every tier of ONE codeword; a CTA holds
-//    G codewords (G*Z threads); tiers run in sequence with one CTA barrier
-//    between them (layered schedule); the Z rows of a tier touch disjoint
-//    columns, so running them concurrently equals the reference's row loop;
-//  * posteriors live in shared memory as [cw][c][j] (c = position inside the
+//    one codeword (ceil(Z/32) warps); tiers run in sequence with one CTA
+//    barrier between them (layered schedule); the Z rows of a tier touch
+//    disjoint columns, so running them concurrently equals the reference's
+//    row loop;
+//  * posteriors live in shared memory as [c][j] (c = position inside the
 //    circulant, j = block column, rows padded to 25 columns); the cyclic
 //    shift of edge (j, e) is the indexed shared-memory read at
 //    ((r + e) mod Z) * 25 + j -- no expanded H anywhere.  For the 18 native
-//    codes Z and the shifts are compile-time constants (one ISETP + one SEL
-//    per edge, circulant offset folded into the LDS immediate); scaled WiMAX
-//    codes take them from the kernel parameter block;
+//    codes Z and the shifts are compile-time constants; scaled WiMAX codes
+//    take them from the kernel parameter block; the per-edge base select is
+//    kept in registers or in a per-thread shared-memory address table,
+//    whichever measured faster for the structure (use_addr_tab);
 //  * the check-to-variable messages of a thread's rows are held explicitly,
 //    one register per edge (the reference keeps them compressed as
 //    min1/min2/argmin/sign bits and rebuilds L_old every sweep,
 //    _kernels.py:62-63; keeping the rebuilt values is bit-identical and
 //    removes that work from the inner loop);
 //  * instruction mix is chosen for the measured pipe rates (tools/pipebench):
-//    FADD is full rate, IMAD / VIADD.16x2 share the half-rate FMA-heavy pipe,
-//    compare / select / logic / min-max share the half-rate ALU pipe and
-//    IMAD.HI is quarter rate, so sign handling rides on IMAD and min/max
-//    are tracked two edges per step with 3-input min.
+//    FADD/FADD2 are full rate, IMAD / VIADD.16x2 share the half-rate
+//    FMA-heavy pipe, compare / select / logic / min-max share the half-rate
+//    ALU pipe and IMAD.HI is quarter rate, so sign handling rides on IMAD and
+//    the leave-one-out minima step two edges at a time with 3-input min.
+//  A persistent variant that prefetched the next codeword's LLRs by bulk
+//  copy was measured slower on C2 (68-74 vs 84 Gb/s: the outer block loop
+//  cost registers and spills), so each CTA decodes one codeword.
 #pragma once
 #include <algorithm>
 #include <cstdlib>
@@ -52,29 +59,6 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
-}
-__device__ __forceinline__ uint32_t imulhi(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
-// acc += bit if z < 0 (exact "< 0": -0.0 and NaN do not count, _kernels.py:73)
-__device__ __forceinline__ void add_if_neg_f32(uint32_t& acc, float z, uint32_t bit, uint32_t one) {
-  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, 0f00000000;\n\t@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
-      : "+r"(acc) : "f"(z), "r"(bit), "r"(one));
-}
-// acc += bit if bit 15 of d is set (int16 "zz < 0", _kernels.py:159)
-__device__ __forceinline__ void add_if_neg_i16(uint32_t& acc, uint32_t d, uint32_t bit, uint32_t one) {
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, 0x8000;\n\tsetp.ne.u32 p, t, 0;\n\t"
-      "@p mad.lo.u32 %0, %2, %3, %0;\n\t}"
-      : "+r"(acc) : "r"(d), "r"(bit), "r"(one));
-}
-// 16-bit signed lane ops on the low halves (high halves are don't-care)
-__device__ __forceinline__ uint32_t vmin16(uint32_t a, uint32_t b) {
-  uint32_t d; asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
-}
-__device__ __forceinline__ uint32_t vmax16(uint32_t a, uint32_t b) {
-  uint32_t d; asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
 }
 
 // packed float32x2 add/sub (FADD2: two IEEE float32 ops in one instruction)
@@ -170,127 +154,6 @@ struct ArithF32 {
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) f_add2(zz[k], zz[k + 1], msg[k], msg[k + 1], o[k], o[k + 1]);
     if (D & 1) o[D - 1] = f_add(zz[D - 1], msg[D - 1]);
-  }
-};
-
-// ---------------------------------------------------------------------------
-// int16 row update (_kernels.py:135-170): two's-complement wrap after every
-// op.  Values are carried in 32-bit registers whose LOW 16 bits are the
-// int16 value; 16-bit shared-memory loads sign-extend and 16-bit stores
-// truncate, so the wrap after add/sub is free; |zz| and the min/max run as
-// s16x2 lane ops on the low half (abs(-32768) = -32768 sorts lowest, exactly
-// the reference's int16 behaviour).  Messages are kept as full int16 values.
-// ---------------------------------------------------------------------------
-#ifndef QCB_I16_LOO_MAXDEG
-#define QCB_I16_LOO_MAXDEG 10
-#endif
-constexpr int kI16LooMaxDeg = QCB_I16_LOO_MAXDEG;
-
-struct ArithI16 {
-  using Val = uint32_t;
-  static constexpr int kElem = 2;
-  static constexpr int kKind = 1;
-
-  __device__ static Val lds(uint32_t a) {
-    short v; asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a)); return (uint32_t)(int)v;
-  }
-  __device__ static void sts(uint32_t a, Val v) {   // stores the low half: the int16 wrap
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-  }
-  __device__ static bool hard(Val v) { return (int)v <= 0; }   // v is sign-extended when it comes from lds
-  __device__ static Val zero() { return 0u; }
-  __device__ static short canon(short v) { return v; }
-
-  // min1/min2 pair formulation (fewer live values than leave-one-out: used
-  // for high-degree rows, where the leave-one-out arrays would spill)
-  template <int D>
-  __device__ __forceinline__ static void row_pair(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
-    uint32_t d[D], a[D];
-    // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      d[k] = imad(msg[k], K.neg1, p[k]);                 // p - L  (FMA pipe)
-      a[k] = vmax16(d[k], imad(d[k], K.neg1, 0u));       // max(zz, -zz) in 16-bit lanes
-    }
-    // sign-product parity = xor of the int16 sign bits (bit 15)
-    uint32_t sx = 0;
-#pragma unroll
-    for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
-    if (D & 1) sx ^= d[D - 1];
-    // min1 / min2 over a (signed int16 order), two edges per step
-    uint32_t nm1 = 0x7FFFu, nm2 = 0x7FFFu;               // 32767 (_kernels.py:142-143)
-#pragma unroll
-    for (int k = 0; k + 1 < D; k += 2) {
-      const uint32_t lo = vmin16(a[k], a[k + 1]), hi = vmax16(a[k], a[k + 1]);
-      nm2 = vmin16(nm2, vmin16(hi, vmax16(nm1, lo)));
-      nm1 = vmin16(nm1, lo);
-    }
-    if (D & 1) {
-      nm2 = vmin16(nm2, vmax16(nm1, a[D - 1]));
-      nm1 = vmin16(nm1, a[D - 1]);
-    }
-    // pass 2: |L_new| = nm2 iff a_k == nm1 (low halves); sign = parity ^ neg_k
-    const bool par = (sx & 0x8000u) != 0;
-    const uint32_t n1s = par ? imad(nm1, K.neg1, 0u) : nm1;   // parity folded in
-    const uint32_t n2s = par ? imad(nm2, K.neg1, 0u) : nm2;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      // a_k == nm1 <=> min(a_k, nm1) == a_k (a_k >= nm1): one VIMNMX with a predicate
-      uint32_t msel;
-      asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t.reg .b16 l0, h0, l1, h1;\n\t"
-          "min.s16x2 t, %1, %2;\n\tmov.b32 {l0, h0}, t;\n\tmov.b32 {l1, h1}, %1;\n\t"
-          "setp.eq.s16 p, l0, l1;\n\tselp.b32 %0, %4, %3, p;\n\t}"
-          : "=r"(msel) : "r"(a[k]), "r"(nm1), "r"(n1s), "r"(n2s));
-      const uint32_t lnew = (d[k] & 0x8000u) ? imad(msel, K.neg1, 0u) : msel;
-      msg[k] = lnew;
-      o[k] = imad(lnew, K.one, d[k]);                     // zz + L_new, wrapped by the 16-bit store
-    }
-  }
-
-  // Leave-one-out formulation as for float32: |L_new_k| = min_{j != k} a_j in
-  // signed int16 order (abs(-32768) = -32768 sorts lowest, as in the
-  // reference); equals the reference's (k == argmin ? min2 : min1).
-  template <int D>
-  __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
-    if constexpr (D > kI16LooMaxDeg) {
-      row_pair<D>(p, o, msg, K);
-      return;
-    }
-    static_assert(D >= 2, "row degree >= 2");
-    uint32_t d[D], a[D];
-    // pass 1: d = post - L_old (low half = np.int16(post - lold)), a = |zz|
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      d[k] = imad(msg[k], K.neg1, p[k]);                 // p - L  (FMA pipe)
-      a[k] = vmax16(d[k], imad(d[k], K.neg1, 0u));       // max(zz, -zz) in 16-bit lanes
-    }
-    // sign-product parity = xor of the int16 sign bits (bit 15)
-    uint32_t sx = 0;
-#pragma unroll
-    for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
-    if (D & 1) sx ^= d[D - 1];
-    // leave-one-out minima (low halves; 32767 = the reference's initial min)
-    uint32_t pre[D], suf[D], ex[D];
-    pre[1] = a[0];
-#pragma unroll
-    for (int k = 2; k < D; ++k) pre[k] = vmin16(pre[k - 1], a[k - 1]);
-    suf[D - 2] = a[D - 1];
-#pragma unroll
-    for (int k = D - 3; k >= 0; --k) suf[k] = vmin16(suf[k + 1], a[k + 1]);
-    ex[0] = suf[0];
-    ex[D - 1] = pre[D - 1];
-#pragma unroll
-    for (int k = 1; k < D - 1; ++k) ex[k] = vmin16(pre[k], suf[k]);
-    // pass 2: L_new = +-ex with sign = parity ^ (zz_k < 0): sigma = +-1 from
-    // bit 15 of (d ^ sx); msg = ex * sigma, post = d + ex * sigma (both IMAD)
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      uint32_t sg;
-      asm("{\n\t.reg .b32 t;\n\txor.b32 t, %1, %2;\n\tprmt.b32 t, t, 0, 0x9999;\n\tor.b32 %0, t, 1;\n\t}"
-          : "=r"(sg) : "r"(d[k]), "r"(sx));
-      msg[k] = imad(ex[k], sg, 0u);
-      o[k] = imad(ex[k], sg, d[k]);                       // zz + L_new, wrapped by the 16-bit store
-    }
   }
 };
 
@@ -602,9 +465,9 @@ constexpr int raise_cap(int z, int want, int cw_smem, bool raise) {
 
 template <class S, class A, int ZS>
 constexpr int reg_cap() {
-  const int want = S::NE + QCB_REG_SLACK + (A::kElem == 2 ? S::MAXDEG : 0);
+  const int want = S::NE + QCB_REG_SLACK;
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, want, (z * kRowStrideUnits * A::kElem + 15) & ~15, A::kElem == 2);
+  return raise_cap(z, want, (z * kRowStrideUnits * A::kElem + 15) & ~15, false);
 }
 
 template <class S, class A, int ZS, bool ET>
@@ -646,23 +509,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 
   // ---- channel LLRs -> [cw][c][j] --------------------------------------------
   {
-    const int nthr = blockDim.x;
-    if constexpr (A::kElem == 4) {
-      load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
-    } else {
-      const int dj = nthr / Z, dc = nthr - dj * Z;
-      for (int q = 0; q < ncw; ++q) {
-        const uint32_t cb = sbase + (uint32_t)q * cws;
-        int j = tid / Z, c = tid - (tid / Z) * Z;
-        const short* src = reinterpret_cast<const short*>(a.llr) + (cw0 + q) * N;
-        for (int n = tid; n < N; n += nthr) {
-          const short v = __ldcs(src + n);
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(cb + c * RS + j * 2), "h"(v));
-          c += dc; j += dj;
-          if (c >= Z) { c -= Z; ++j; }
-        }
-      }
-    }
+    load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -708,62 +555,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
-  if constexpr (A::kElem == 4) {
-    uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
-    float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
-    store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
-                         [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
-                         [](uint32_t v) { return __uint_as_float(v); });
-    return;
-  }
-  const int nthr = blockDim.x;
-  if (a.hard_packed) {
-    const int nbytes = (N + 7) >> 3;
-    uint8_t* hp = reinterpret_cast<uint8_t*>(a.hard) + cw0 * nbytes;
-    for (int i = tid; i < ncw * nbytes; i += nthr) {
-      const int q = i / nbytes, b = i - q * nbytes;
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      uint32_t byte = 0;
-      int n = b * 8;
-      int j = n / Z, c = n - j * Z;
-#pragma unroll
-      for (int u = 0; u < 8; ++u, ++n) {
-        const bool h = n < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
-        byte = (byte << 1) | (h ? 1u : 0u);
-        if (++c == Z) { c = 0; ++j; }
-      }
-      hp[i] = (uint8_t)byte;
-    }
-  } else {
-    uint8_t* h = reinterpret_cast<uint8_t*>(a.hard) + cw0 * N;
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      for (int n4 = tid * 4; n4 < N; n4 += nthr * 4) {
-        int j = n4 / Z, c = n4 - j * Z;
-        uint32_t word = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool hb = (n4 + u) < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
-          word |= (hb ? 1u : 0u) << (8 * u);
-          if (++c == Z) { c = 0; ++j; }
-        }
-        uint8_t* dst = h + (int64_t)q * N + n4;
-        if (n4 + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) *reinterpret_cast<uint32_t*>(dst) = word;
-        else for (int u = 0; n4 + u < N; ++u) dst[u] = (uint8_t)(word >> (8 * u));
-      }
-    }
-  }
-  if (a.post) {
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      for (int n = tid; n < N; n += nthr) {
-        const int j = n / Z, c = n - j * Z;
-        const Val v = A::lds(cb + c * RS + j * A::kElem);
-        if constexpr (A::kElem == 4) reinterpret_cast<float*>(a.post)[(cw0 + q) * N + n] = v;
-        else reinterpret_cast<int16_t*>(a.post)[(cw0 + q) * N + n] = (int16_t)v;
-      }
-    }
-  }
+  uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
+  float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
+  store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
+                       [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
+                       [](uint32_t v) { return __uint_as_float(v); });
 }
 
 // codewords per CTA for a kernel with `regs` registers per thread

@@ -26,7 +26,7 @@ cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStrea
 }
 
 int spec_row_stride_bytes(int elem) {
-  return elem == 4 ? row_stride_bytes<ArithF32>() : row_stride_bytes<ArithI16>();
+  return kRowStrideUnits * elem;
 }
 
 int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w, 128, 4); }
@@ -52,16 +52,10 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   *pair16 = 0;
 
   if (elem == 2) {                          // int16: two codewords per thread in 16x2 lanes
-    static const bool pair_off = [] {
-      const char* p = getenv("QCB_I16_PAIR");
-      return p && p[0] == '0';
-    }();
-    if (!pair_off) {
-      *pair16 = 1;
-      *cw_per_cta = 1;                      // planned at launch from the kernel's registers
-      *tmem_cols = 0;
-      return;
-    }
+    *pair16 = 1;
+    *cw_per_cta = 1;                        // planned at launch from the kernel's registers
+    *tmem_cols = 0;
+    return;
   }
 #define QCB_NE(STRUCT) if (structure_id == STRUCT::ID) { ne = STRUCT::NE; maxdeg = STRUCT::MAXDEG; }
   QCB_FOR_EACH_STRUCTURE(QCB_NE)

@@ -17,6 +17,7 @@ struct KernelFacts {
   cudaFuncAttributes attr{};
   bool have_attr = false;
   int dyn_smem = -1;      // largest MaxDynamicSharedMemorySize set so far
+  int occ_threads = -1, occ_smem = -1, occ = 0;   // last occupancy query
 };
 
 inline std::mutex& launch_cache_mutex() {
@@ -70,6 +71,23 @@ inline cudaError_t ensure_dyn_smem(const void* k, size_t bytes) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e == cudaSuccess) f.dyn_smem = (int)bytes;
   return e;
+}
+
+// resident CTAs per SM for (threads, dynamic smem) (queried once per shape)
+inline cudaError_t kernel_occupancy(const void* k, int threads, size_t smem, int* out) {
+  const auto key = std::make_pair(k, current_device());
+  std::lock_guard<std::mutex> lk(launch_cache_mutex());
+  KernelFacts& f = launch_cache()[key];
+  if (f.occ_threads != threads || f.occ_smem != (int)smem) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+    if (e != cudaSuccess) return e;
+    f.occ_threads = threads;
+    f.occ_smem = (int)smem;
+    f.occ = occ;
+  }
+  *out = f.occ;
+  return cudaSuccess;
 }
 
 }  // namespace qcb
