@@ -486,10 +486,17 @@ def run_e2e(args, wl, mms, llrs, world, dist, dev):
     step()
     if dist:
         dist.barrier()
-    t0 = time.perf_counter()
+    # device-side timing: events on the (idle) default stream bracket the
+    # blocking host calls, whose copies and kernels run on the library's own
+    # streams; the elapsed time is read from the GPU clock, max over ranks
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(torch.cuda.default_stream(dev))
     for _ in range(steps):
         step()
-    dt = time.perf_counter() - t0
+    e1.record(torch.cuda.default_stream(dev))
+    e1.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3
     t = torch.tensor([dt], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
