@@ -339,6 +339,45 @@ struct EarlyMask { static constexpr uint32_t value = early_mask_of<S, T>(); };
 template <class S, int T>
 __device__ __forceinline__ constexpr bool early_edge(int k) { return (EarlyMask<S, T>::value >> k) & 1u; }
 
+// Shared-memory message slots: the messages of the first SMT tiers can live in
+// shared memory instead of registers (whole tiers, 16-byte aligned per tier,
+// an odd number of 16-byte units per thread so quarter-warp LDS.128 / STS.128
+// are conflict-free); fewer registers per thread, more resident CTAs.
+// Measured on B200 (C2 / C4 / C1 Gb/s): SMT = 0: 83.7 / 58.2 / 29.5;
+// 2: 78.8 / 54.6 / 28.8; 4 (7 CTAs/SM instead of 5): 74.5 / 48.2 / 29.0;
+// 6: 70.0 / 42.3 / 26.8 -- the row update is not occupancy-bound, so the
+// default keeps every message in registers.
+#ifndef QCB_SMEM_MSG_TIERS
+#define QCB_SMEM_MSG_TIERS 0
+#endif
+template <class S>
+struct SmemMsg {
+  static constexpr int SMT = QCB_SMEM_MSG_TIERS < S::MB ? QCB_SMEM_MSG_TIERS : S::MB;
+  static constexpr int r4(int d) { return (d + 3) / 4 * 4; }
+  static constexpr int off(int t) {            // word offset of tier t's slots
+    int o = 0;
+    for (int i = 0; i < t; ++i) o += r4(S::DEG[i]);
+    return o;
+  }
+  static constexpr int words() {                // per-thread stride in words (0 if unused)
+    const int w = off(SMT);
+    if (w == 0) return 0;
+    int u = w / 4;
+    if ((u & 1) == 0) ++u;
+    return 4 * u;
+  }
+  static constexpr int in_regs() { return S::NE - S::START[SMT]; }   // messages still in registers
+};
+
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128f(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+
 template <class S, class A, int ZS>
 struct Layered {
   using Val = typename A::Val;
@@ -351,7 +390,7 @@ struct Layered {
   // tier T+1's early posteriors (early_edge) before the barrier
   template <int T>
   __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                              uint32_t tab, Val (&msg)[S::NE], Val (&pe)[S::MAXDEG],
+                                              uint32_t tab, uint32_t mbase, Val (&msg)[S::NE], Val (&pe)[S::MAXDEG],
                                               Val (&pn)[S::MAXDEG], uint32_t (&ec)[ME], uint32_t (&en)[ME]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
@@ -361,7 +400,21 @@ struct Layered {
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
     tab_fetch<S, ZS, TAB, T + 1>(tab, en);
-    A::template row<D>(p, o, msg + E0, K);
+    if constexpr (T < SmemMsg<S>::SMT) {
+      constexpr int D4 = SmemMsg<S>::r4(D);
+      const uint32_t ma = mbase + (uint32_t)(SmemMsg<S>::off(T) * 4);
+      Val m[D4];
+#pragma unroll
+      for (int q = 0; q < D4 / 4; ++q) {
+        const float4 v = lds128f(ma + 16u * q);
+        m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
+      }
+      A::template row<D>(p, o, m, K);
+#pragma unroll
+      for (int q = 0; q < D4 / 4; ++q) sts128f(ma + 16u * q, m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+    } else {
+      A::template row<D>(p, o, msg + E0, K);
+    }
 #pragma unroll
     for (int k = 0; k < D; ++k) A::sts(addr[k], o[k]);
     if constexpr (T + 1 < S::MB && EarlyMask<S, T + 1>::value != 0) {
@@ -390,19 +443,19 @@ struct Layered {
   // the batch work on scratch / unused slots): no branch around the tier body
   template <bool ET, int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                               uint32_t tab, Val (&msg)[S::NE], bool work,
+                                               uint32_t tab, uint32_t mbase, Val (&msg)[S::NE], bool work,
                                                std::integer_sequence<int, Ts...>) {
     Val pa[S::MAXDEG], pb[S::MAXDEG];
     uint32_t ea[ME], eb[ME];
     tab_fetch<S, ZS, TAB, 0>(tab, ea);
     if constexpr (ET) {
-      ((work ? tier<Ts>(a, K, r, b0, b1, tab, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
-                        (Ts & 1) ? ea : eb)
+      ((work ? tier<Ts>(a, K, r, b0, b1, tab, mbase, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
+                        (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
              : void(),
         __syncthreads()), ...);
     } else {
       (void)work;
-      ((tier<Ts>(a, K, r, b0, b1, tab, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
+      ((tier<Ts>(a, K, r, b0, b1, tab, mbase, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
                  (Ts & 1) ? ea : eb),
         __syncthreads()), ...);
     }
@@ -465,7 +518,7 @@ constexpr int raise_cap(int z, int want, int cw_smem, bool raise) {
 
 template <class S, class A, int ZS>
 constexpr int reg_cap() {
-  const int want = S::NE + QCB_REG_SLACK;
+  const int want = SmemMsg<S>::in_regs() + QCB_REG_SLACK;
   const int z = ZS > 0 ? ZS : 96;
   return raise_cap(z, want, (z * kRowStrideUnits * A::kElem + 15) & ~15, false);
 }
@@ -506,6 +559,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   // this thread's address table (after the G posterior blocks)
   const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
   fill_addr_tab<S, A, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
+  // this thread's shared-memory message slots (first SMT tiers), after the tables
+  const uint32_t mbase = ((sbase + (uint32_t)G * cws + blockDim.x * (uint32_t)addr_tab_bytes_per_thread<S, ZS, L::TAB>()
+                           + 15u) & ~15u) + (uint32_t)(tid * SmemMsg<S>::words() * 4);
+#pragma unroll
+  for (int q = 0; q < SmemMsg<S>::words() / 4; ++q) sts128f(mbase + 16u * q, 0.0f, 0.0f, 0.0f, 0.0f);
 
   // ---- channel LLRs -> [cw][c][j] --------------------------------------------
   {
@@ -523,7 +581,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   if constexpr (!ET) {
     // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
-    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, msg, act, tiers);
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, mbase, msg, act, tiers);
     if (a.max_iters > 0) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
@@ -534,7 +592,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   } else {
     for (int k = 0; k < a.max_iters; ++k) {
       const bool work = act && !s_done[gs];
-      L::template sweep<true>(a, K, rs, b0, b1, tab, msg, work, tiers);
+      L::template sweep<true>(a, K, rs, b0, b1, tab, mbase, msg, work, tiers);
       if (tid < kLayMaxCw) s_fail[tid] = 0;     // syndrome (_kernels.py:85-96)
       __syncthreads();
       if (work && L::parity_all(a, rs, b0, b1, tab, tiers)) s_fail[gs] = 1;
@@ -575,9 +633,11 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
 }
 
 template <class K>
-inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0) {
+inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0,
+                                        int msg_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)a.pairs * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes;
+  const size_t smem = (((size_t)a.pairs * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
+                      (size_t)threads * msg_bytes;
   cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
@@ -600,7 +660,8 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
-  return launch_layered_fixed(kern, b, z, RS, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>());
+  return launch_layered_fixed(kern, b, z, RS, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
+                              SmemMsg<S>::words() * 4);
 }
 
 }  // namespace qcb
