@@ -73,6 +73,46 @@ __device__ __forceinline__ void f_add2(float a0, float a1, float b0, float b1, f
       : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 
+// Leave-one-out minima ex[k] = min_{j != k} a[j] with prefix / suffix minima
+// kept only at "anchor" positions two edges apart (3-input mins) and the
+// remaining terms folded into each ex[k]: 2D - 2 mins for even D instead of
+// 3D - 6 (D = 14: 26 vs 36).  `inf` seeds the anchors (int16: 32767, the
+// reference's initial min, which every |zz| <= 32767 beats).  Used by the
+// int16 kernel where measured faster (WiMAX structures: C5 +1.4 %; Wi-Fi 1944
+// R5/6 -2.7 %, float32 C2 flat).
+template <int D, class V, class Min>
+__device__ __forceinline__ void loo_minima(const V (&a)[D], V (&ex)[D], Min mn, V inf) {
+  static_assert(D >= 2, "row degree >= 2");
+  if constexpr (D == 2) {
+    ex[0] = mn(a[1], inf);
+    ex[1] = mn(a[0], inf);
+  } else {
+    V P[D + 1], S[D + 1];
+    P[2] = mn(mn(a[0], a[1]), inf);                       // P[k] = min a[0..k-1], k even
+#pragma unroll
+    for (int k = 4; k <= D - 1; k += 2) P[k] = mn(mn(P[k - 2], a[k - 2]), a[k - 1]);
+    S[D - 3] = mn(mn(a[D - 2], a[D - 1]), inf);           // S[k] = min a[k+1..D-1], D-1-k even
+#pragma unroll
+    for (int k = D - 5; k >= 0; k -= 2) S[k] = mn(mn(S[k + 2], a[k + 2]), a[k + 1]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      // prefix part: none (k = 0) | a0 (k = 1) | P[k] (k even) | P[k-1], a[k-1]
+      // suffix part: none (k = D-1) | a[D-1] (k = D-2) | S[k] (D-1-k even) | S[k+1], a[k+1]
+      const bool p_anchor = k >= 2, s_anchor = k <= D - 3;
+      V v;
+      if (k == 0) v = ((D - 1) % 2 == 0) ? S[0] : mn(S[1], a[1]);
+      else if (k == D - 1) v = (k % 2 == 0) ? P[k] : mn(P[k - 1], a[k - 1]);
+      else {
+        const V pp = (k == 1) ? a[0] : ((k % 2 == 0) ? P[k] : mn(P[k - 1], a[k - 1]));
+        const V ss = (k == D - 2) ? a[D - 1] : (((D - 1 - k) % 2 == 0) ? S[k] : mn(S[k + 1], a[k + 1]));
+        v = mn(pp, ss);
+        if (!p_anchor && !s_anchor) v = mn(v, inf);       // D = 3, k = 1: no seeded anchor involved
+      }
+      ex[k] = v;
+    }
+  }
+}
+
 struct RtK {              // runtime constants (kernel parameters)
   uint32_t one, sign, shr, neg1, lane1;   // lane1 = 0x00010001 (16x2 kernels)
 };

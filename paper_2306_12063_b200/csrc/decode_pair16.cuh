@@ -53,7 +53,7 @@ struct ArithI16x2 {
 
   // One row of D edges: posteriors p[] in, new posteriors o[] out, negated
   // messages nm[] updated in place (both codewords' lanes).
-  template <int D>
+  template <int D, bool ANCHOR = false>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* nm, const RtK& K) {
     static_assert(D >= 2, "row degree >= 2");
     uint32_t d[D], a[D];
@@ -66,24 +66,31 @@ struct ArithI16x2 {
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
     if (D & 1) sx ^= d[D - 1];
-    // suffix / prefix chains step two edges at a time (VIMNMX3.S16x2)
-    uint32_t suf[D], pre[D];
-    suf[D - 2] = a[D - 1];
+    uint32_t exa[D];
+    if constexpr (ANCHOR) {
+      loo_minima<D>(a, exa, [](uint32_t x, uint32_t y) { return vmin2(x, y); }, 0x7FFF7FFFu);
+    } else {
+      // suffix / prefix chains step two edges at a time (VIMNMX3.S16x2)
+      uint32_t suf[D], pre[D];
+      suf[D - 2] = a[D - 1];
 #pragma unroll
-    for (int k = D - 3; k >= 0; --k) {
-      const int m = D - 1 - k;
-      if (k == D - 3 || (m & 1)) suf[k] = vmin2(suf[k + 1], a[k + 1]);
-      else suf[k] = vmin2(vmin2(suf[k + 2], a[k + 2]), a[k + 1]);
-    }
-    pre[1] = a[0];
+      for (int k = D - 3; k >= 0; --k) {
+        const int m = D - 1 - k;
+        if (k == D - 3 || (m & 1)) suf[k] = vmin2(suf[k + 1], a[k + 1]);
+        else suf[k] = vmin2(vmin2(suf[k + 2], a[k + 2]), a[k + 1]);
+      }
+      pre[1] = a[0];
 #pragma unroll
-    for (int k = 2; k < D; ++k) {
-      if (k == 2 || (k & 1)) pre[k] = vmin2(pre[k - 1], a[k - 1]);
-      else pre[k] = vmin2(vmin2(pre[k - 2], a[k - 2]), a[k - 1]);
+      for (int k = 2; k < D; ++k) {
+        if (k == 2 || (k & 1)) pre[k] = vmin2(pre[k - 1], a[k - 1]);
+        else pre[k] = vmin2(vmin2(pre[k - 2], a[k - 2]), a[k - 1]);
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) exa[k] = k == 0 ? suf[0] : (k == D - 1 ? pre[D - 1] : vmin2(pre[k], suf[k]));
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const uint32_t ex = k == 0 ? suf[0] : (k == D - 1 ? pre[D - 1] : vmin2(pre[k], suf[k]));
+      const uint32_t ex = exa[k];
       const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
       const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
       o[k] = vadd2(d[k], (nex & m) | (ex & ~m));                   // post = zz + L_new
@@ -114,7 +121,7 @@ struct Layered2 {
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
     tab_fetch<S, ZS, TAB, T + 1>(tab, en);
-    A::template row<D>(p, o, nm + E0, K);
+    A::template row<D, (S::ID >= 12)>(p, o, nm + E0, K);   // anchor minima on the WiMAX structures
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       uint32_t v = o[k];
