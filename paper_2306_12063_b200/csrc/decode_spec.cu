@@ -29,7 +29,6 @@ int spec_row_stride_bytes(int elem) {
   return kRowStrideUnits * elem;
 }
 
-int spec_cw_per_cta(int z, int64_t w) { return layered_cw_per_cta(z, w, 128, 4); }
 
 // Choose between the register-resident and the TMEM-resident message store.
 // QCB_TMEM=0/1 forces one (benchmarks); default: TMEM when it keeps more
