@@ -220,7 +220,7 @@ def run_reference(args, wl):
         "impl": "reference", "metric": f"decoded coded Gbit/s ({wl.key}, fixed {wl.iters} iters)",
         "value": round(value, 6), "unit": "Gbit/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None,
         "dtype": "int16" if wl.fixed else "f32", "data": "synthetic (seeded BPSK/AWGN, reference recipe)",
         "config": config_dict(wl, args),
         "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads, "kind": "port",
@@ -235,11 +235,14 @@ def run_reference(args, wl):
         dist.destroy_process_group()
 
 
-def config_dict(wl, args):
+def config_dict(wl, args, job=None, world=1):
     from paper_2306_12063_b200 import codebook as CB
+    job = job or wl
     names = [f"{c[0]}-{c[1]}-r{c[2].replace('/', '')}" for c in wl.codes]
     return {"workload": f"{wl.key}: " + (names[0] if len(names) == 1 else f"{len(names)} codes mixed"),
-            "codewords_per_gpu": wl.w_total, "n_bits": CB.get_model_matrix(*wl.codes[0]).n,
+            "codewords_per_gpu": wl.w_total,
+            "codewords_total": job.w_total if job.strong else wl.w_total * world,
+            "n_bits": CB.get_model_matrix(*wl.codes[0]).n,
             "iterations": wl.iters, "early_termination": False, "ebn0_db": wl.ebn0_db,
             "arithmetic": wl.arithmetic.value, "parallelism": f"dp{args.gpus} (codeword shards)",
             "launch": "direct" if getattr(args, "no_graph", False) or getattr(args, "impl", "ours") == "reference"
@@ -263,6 +266,8 @@ def run_ours(args, wl):
     from paper_2306_12063_b200 import _lib
     from paper_2306_12063_b200.workloads import device_llrs
     _lib.lib()
+    job = wl
+    wl = wl.for_rank(rank, world)                 # this rank's share of the job
     cfg = wl.config()
     mms = wl.model_matrices()
     codes = [P.code_handle(mm) for mm in mms]
@@ -334,7 +339,7 @@ def run_ours(args, wl):
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     elapsed_ms = float(t_max.item())
     ms_per_step = elapsed_ms / args.steps
-    bits_per_step = coded_bits(wl) * world
+    bits_per_step = coded_bits(job) if job.strong else coded_bits(wl) * world
     value = bits_per_step / (ms_per_step * 1e-3) / 1e9
 
     # counters (bit/frame errors vs the transmitted codewords, iterations) -> one NCCL all_reduce
@@ -369,7 +374,7 @@ def run_ours(args, wl):
     if wl.key == "C5" and not args.no_encode:
         del llrs, outs
         torch.cuda.empty_cache()
-        enc = run_encode(args, wl, mms[0], dev, dist)
+        enc = run_encode(args, wl, mms[0], dev, dist, job.w_per_code if job.strong else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
@@ -383,9 +388,10 @@ def run_ours(args, wl):
             "metric": f"decoded coded Gbit/s ({wl.key}, fixed {wl.iters} iters)",
             "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int16" if wl.fixed else "f32",
+            "scaling": "strong" if job.strong else "weak", "vs_baseline": None,
+            "dtype": "int16" if wl.fixed else "f32",
             "data": "synthetic (seeded BPSK/AWGN LLRs, reference channel recipe)",
-            "config": config_dict(wl, args),
+            "config": config_dict(wl, args, job, world),
             "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(alu_peak, 3),
                          "unit": "Tops/s", "frac": round(achieved / alu_peak, 4),
                          "traffic": traffic,
@@ -400,7 +406,7 @@ def run_ours(args, wl):
             "clocks": clocks.summary(),
             "counters": {"bit_errors": cnt[0], "frame_errors": cnt[1], "iter_sum": cnt[2],
                          "converged": cnt[3], "frames": cnt[4],
-                         "ber": cnt[0] / max(1, wl.w_total * world * mms[0].k)},
+                         "ber": cnt[0] / max(1, cnt[4] * mms[0].k)},
         }
         if e2e:
             line["e2e"] = e2e
@@ -414,7 +420,7 @@ def run_ours(args, wl):
         dist.destroy_process_group()
 
 
-def run_encode(args, wl, mm, dev, dist):
+def run_encode(args, wl, mm, dev, dist, job_w=None):
     """BASELINE config 5, second half: bit-packed direct encoding of 2^22 seeded
     info words (K = 1728 bits) on the GPU; HBM-bound (216 B in + 288 B out per
     codeword).  A sample is checked against the CPU oracle."""
@@ -453,7 +459,7 @@ def run_encode(args, wl, mm, dev, dist):
     idx = torch.randint(0, w, (1024,), device=dev, generator=g)
     ok = bool(np.array_equal(out[idx].cpu().numpy(), O.encode_packed(mm, info[idx].cpu().numpy())))
     return {"metric": "encoded coded Gbit/s (C5, 2^22 x K=1728 info words)",
-            "value": round(w * mm.n * world / (ms * 1e-3) / 1e9, 2), "unit": "Gbit/s",
+            "value": round((job_w if job_w else w * world) * mm.n / (ms * 1e-3) / 1e9, 2), "unit": "Gbit/s",
             "ms_per_step": round(ms, 4), "codewords_per_gpu": w, "gpu_launches": steps,
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks.get("hbm_gbs"),
                          "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs", 6650.0), 4),

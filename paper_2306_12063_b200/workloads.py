@@ -41,6 +41,7 @@ class Workload:
     w_per_code: int
     ebn0_db: float
     seed: int
+    strong: bool = False    # True: w_per_code is the job total, sharded over the ranks
 
     @property
     def arithmetic(self) -> Arithmetic:
@@ -57,6 +58,16 @@ class Workload:
     def w_total(self) -> int:
         return self.w_per_code * len(self.codes)
 
+    def for_rank(self, rank: int, world: int) -> "Workload":
+        """This rank's share: the whole per-GPU batch (weak scaling) or its
+        contiguous shard of the job total (strong scaling, shard.shard_range)."""
+        if not self.strong or world == 1:
+            return self
+        from dataclasses import replace
+        from .shard import shard_range
+        lo, hi = shard_range(self.w_per_code, rank, world)
+        return replace(self, w_per_code=hi - lo)
+
 
 ALL_18 = tuple([("wifi", n, r) for n in (648, 1296, 1944) for r in ("1/2", "2/3", "3/4", "5/6")]
                + [("wimax", 2304, r) for r in ("1/2", "2/3A", "2/3B", "3/4A", "3/4B", "5/6")])
@@ -66,7 +77,8 @@ WORKLOADS = {
     "C2": Workload("C2", (("wimax", 2304, "1/2"),), False, 10, 65536, 1.5, 2),
     "C3": Workload("C3", (("wifi", 1944, "5/6"),), True, 8, 262144, 4.0, 3),
     "C4": Workload("C4", ALL_18, False, 10, 16384, 3.0, 4),
-    "C5": Workload("C5", (("wimax", 2304, "3/4A"),), True, 10, 1 << 22, 2.0, 5),
+    # BASELINE config 5: 2^22 codewords sharded across 1/2/4/8 GPUs (strong scaling)
+    "C5": Workload("C5", (("wimax", 2304, "3/4A"),), True, 10, 1 << 22, 2.0, 5, True),
 }
 
 

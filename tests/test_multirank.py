@@ -70,3 +70,14 @@ def test_counters_all_reduce_over_two_gloo_ranks():
     conv = torch.randint(0, 2, (w,), dtype=torch.uint8, generator=g)
     want = shard.decode_counters(hard, iters, conv, info, k).tolist()
     assert got == want and got[4] == w
+
+
+def test_strong_scaling_workload_shards_cover_the_job():
+    from paper_2306_12063_b200.workloads import WORKLOADS
+    c5 = WORKLOADS["C5"]
+    assert c5.strong
+    for world in (1, 2, 3, 4, 8):
+        parts = [c5.for_rank(r, world).w_per_code for r in range(world)]
+        assert sum(parts) == c5.w_per_code and max(parts) - min(parts) <= 1
+    c2 = WORKLOADS["C2"]
+    assert not c2.strong and c2.for_rank(3, 8).w_per_code == c2.w_per_code
