@@ -257,16 +257,64 @@ def _walk_batches(sums: np.ndarray, counts: list[int], state: list[int], min_err
     return False
 
 
+def _point_distributed(chunk_sums, chunk: int, max_frames: int, min_errors: int, min_frames: int,
+                       group=None, device=None) -> list[int]:
+    """One SNR point's frame loop over consecutive `chunk`-frame chunks.
+
+    `chunk_sums(f0, count)` returns the (ceil(count/256), 3) int64 per-batch
+    counters of frames [f0, f0+count).  With a torch.distributed group of W
+    ranks, rank r computes chunks r, r+W, ... of each round, the rounds'
+    counters are all-gathered (the path's only collective) and every rank walks
+    the batches in frame order with the reference's stop rule -- so the
+    result is identical for any number of ranks.  Returns [frames, bit_errors,
+    frame_errors, iter_sum]."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    nb = chunk // BATCH_FRAMES
+    state = [0, 0, 0, 0]                          # frames, bit_errors, frame_errors, iter_sum
+    start = 0                                     # first frame of this round
+    while True:
+        if max_frames - start <= 0:
+            break
+        f0 = start + rank * chunk
+        count = max(0, min(chunk, max_frames - f0))
+        mine = torch.zeros((nb, 3), dtype=torch.int64, device=device)
+        if count > 0:
+            s = chunk_sums(f0, count)
+            mine[: s.shape[0]] = s
+        if world > 1:
+            allc = torch.empty((world * nb, 3), dtype=torch.int64, device=device)
+            dist.all_gather_into_tensor(allc, mine, group=group)
+        else:
+            allc = mine
+        sums = allc.cpu().numpy()
+        counts = []
+        for r in range(world):
+            c_r = max(0, min(chunk, max_frames - (start + r * chunk)))
+            counts += [max(0, min(BATCH_FRAMES, c_r - b * BATCH_FRAMES)) for b in range(nb)]
+        # batches past max_frames have count 0: the reference loop has stopped there
+        n_valid = sum(1 for c in counts if c > 0)
+        if _walk_batches(sums[:n_valid], counts[:n_valid], state, min_errors, min_frames):
+            break
+        start += world * chunk
+    return state
+
+
 def run_waterfall(code: ModelMatrix, cfg: DecoderConfig, snrs_db, min_errors: int = 10000,
                   max_frames: int = 1_000_000, seed: int = 0, workers: int = 1, min_frames: int = 1,
                   pool: str = "simple", *, frames: str = "device", chunk_frames: int = 1 << 16,
-                  device=None) -> WaterfallTable:
+                  device=None, group=None) -> WaterfallTable:
     """Simulate info->encode->BPSK->AWGN->LLR->decode per SNR point on the GPU.
 
     A point stops at the first 256-frame batch boundary where bit_errors >=
     min_errors and frames >= min_frames, or when frames reaches max_frames
     (the reference's rule).  `workers` / `pool` are accepted for signature
-    compatibility; the device replaces the worker pool."""
+    compatibility; the device replaces the worker pool.  Under
+    torch.distributed (one process per GPU) pass `group` (e.g.
+    torch.distributed.group.WORLD): the chunks of frames are spread over the
+    group's ranks and the table is the same as on one GPU."""
     import torch
     if min_errors < 1:
         raise ValueError("min_errors must be >= 1")
@@ -279,12 +327,8 @@ def run_waterfall(code: ModelMatrix, cfg: DecoderConfig, snrs_db, min_errors: in
     points = []
     for p_idx, ebn0 in enumerate(snrs_db):
         sigma2 = ebn0_to_sigma2(ebn0, code.rate.fraction)
-        state = [0, 0, 0, 0]                      # frames, bit_errors, frame_errors, iter_sum
-        while True:
-            count = min(chunk, max_frames - state[0])
-            if count <= 0:
-                break
-            f0 = state[0]
+
+        def chunk_sums(f0, count, p_idx=p_idx, sigma2=sigma2):
             if frames == "device":
                 info = frames_info_device(seed, p_idx, f0, count, code.k, dev)
                 noise = None
@@ -296,10 +340,9 @@ def run_waterfall(code: ModelMatrix, cfg: DecoderConfig, snrs_db, min_errors: in
             llr = channel_llr_device(cw, sigma2, cfg.arithmetic, q_b=cfg.q_b, noise=noise, seed=seed,
                                      point=p_idx, frame0=f0)
             hard, iters, _ = decode_batch(code, llr, cfg)
-            sums = count_errors_device(hard, info, iters, code.k).cpu().numpy()
-            counts = [min(BATCH_FRAMES, count - b * BATCH_FRAMES) for b in range(sums.shape[0])]
-            if _walk_batches(sums, counts, state, min_errors, min_frames):
-                break
+            return count_errors_device(hard, info, iters, code.k)
+
+        state = _point_distributed(chunk_sums, chunk, max_frames, min_errors, min_frames, group=group, device=dev)
         fr = state[0]
         points.append(WaterfallPoint(ebn0_db=float(ebn0), frames=fr, bits_decoded=fr * code.k,
                                      bit_errors=state[1], frame_errors=state[2],
