@@ -167,14 +167,13 @@ struct LayeredTm {
 #endif
 template <class S, class A>
 constexpr int tm_reg_cap() {
-  constexpr int want = QCB_TM_REG_BASE + (A::kElem == 2 ? 6 : 5) * S::MAXDEG;
+  constexpr int want = QCB_TM_REG_BASE + 5 * S::MAXDEG;
   return (want + 7) / 8 * 8 > 255 ? 255 : (want + 7) / 8 * 8;
 }
 
 template <class S, class A, int ZS, bool ET>
 __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>()))
     decode_tmem_kernel(const __grid_constant__ SpecArgs a) {
-  using L = Layered<S, A, ZS>;
   using LT = LayeredTm<S, A, ZS>;
   constexpr int RS = row_stride_bytes<A>();
   extern __shared__ __align__(16) unsigned char smem[];
@@ -206,30 +205,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   }
 
   // ---- channel LLRs -> [cw][c][j] ------------------------------------------------
+  static_assert(A::kElem == 4, "float32 cells");
   {
-    const int nthr = blockDim.x;
-    const int dj = nthr / Z, dc = nthr - dj * Z;
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      int j = tid / Z, c = tid - (tid / Z) * Z;
-      if constexpr (A::kElem == 4) {
-        const float* src = reinterpret_cast<const float*>(a.llr) + (cw0 + q) * N;
-        for (int n = tid; n < N; n += nthr) {
-          const float v = A::canon(__ldcs(src + n));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(cb + c * RS + j * 4), "f"(v));
-          c += dc; j += dj;
-          if (c >= Z) { c -= Z; ++j; }
-        }
-      } else {
-        const short* src = reinterpret_cast<const short*>(a.llr) + (cw0 + q) * N;
-        for (int n = tid; n < N; n += nthr) {
-          const short v = __ldcs(src + n);
-          asm volatile("st.shared.b16 [%0], %1;" ::"r"(cb + c * RS + j * 2), "h"(v));
-          c += dc; j += dj;
-          if (c >= Z) { c -= Z; ++j; }
-        }
-      }
-    }
+    load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -256,25 +234,33 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   tm_ld_n<S::START[0], S::DEG[0]>(tb, bufA);    // prefetch tier 0
 
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
-  for (int k = 0; k < a.max_iters; ++k) {
-    const bool work = act && !(ET && s_done[g]);
-    LT::sweep(a, K, r, b0, b1, tb, bufA, bufB, work, tiers);
-    const bool last = (k + 1 == a.max_iters);
-    if (ET || last) {
+  if constexpr (!ET) {
+    // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
+    for (int k = 0; k < a.max_iters; ++k) LT::sweep(a, K, r, b0, b1, tb, bufA, bufB, act, tiers);
+    if (a.max_iters > 0) {
       if (tid < kLayMaxCw) s_fail[tid] = 0;
       __syncthreads();
-      if (work && LT::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
+      if (act && LT::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
       __syncthreads();
     }
-    if (tid == 0) s_active = 0;
-    __syncthreads();
-    if (tid < ncw && !s_done[tid]) {
-      s_iters[tid] = k + 1;
-      if (ET && !s_fail[tid]) s_done[tid] = 1;
-      else s_active = 1;
+    if (tid < ncw) s_iters[tid] = a.max_iters;
+  } else {
+    for (int k = 0; k < a.max_iters; ++k) {
+      const bool work = act && !s_done[g];
+      LT::sweep(a, K, r, b0, b1, tb, bufA, bufB, work, tiers);
+      if (tid < kLayMaxCw) s_fail[tid] = 0;       // syndrome (_kernels.py:85-96)
+      __syncthreads();
+      if (work && LT::parity_all(a, r, b0, b1, tiers)) s_fail[g] = 1;
+      if (tid == 0) s_active = 0;
+      __syncthreads();
+      if (tid < ncw && !s_done[tid]) {
+        s_iters[tid] = k + 1;
+        if (!s_fail[tid]) s_done[tid] = 1;
+        else s_active = 1;
+      }
+      __syncthreads();
+      if (!s_active) break;
     }
-    __syncthreads();
-    if (!s_active) break;
   }
   tm_wait_st();
   tm_wait_ld<S::DEG[0]>(bufA);                  // drain the last prefetch
@@ -284,54 +270,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
-  const int nthr = blockDim.x;
-  if (a.hard_packed) {
-    const int nbytes = (N + 7) >> 3;
-    uint8_t* hp = reinterpret_cast<uint8_t*>(a.hard) + cw0 * nbytes;
-    for (int i = tid; i < ncw * nbytes; i += nthr) {
-      const int q = i / nbytes, b = i - q * nbytes;
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      uint32_t byte = 0;
-      int n = b * 8;
-      int j = n / Z, c = n - j * Z;
-#pragma unroll
-      for (int u = 0; u < 8; ++u, ++n) {
-        const bool h = n < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
-        byte = (byte << 1) | (h ? 1u : 0u);
-        if (++c == Z) { c = 0; ++j; }
-      }
-      hp[i] = (uint8_t)byte;
-    }
-  } else {
-    uint8_t* h = reinterpret_cast<uint8_t*>(a.hard) + cw0 * N;
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      for (int n4 = tid * 4; n4 < N; n4 += nthr * 4) {
-        int j = n4 / Z, c = n4 - j * Z;
-        uint32_t word = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool hb = (n4 + u) < N && A::hard(A::lds(cb + c * RS + j * A::kElem));
-          word |= (hb ? 1u : 0u) << (8 * u);
-          if (++c == Z) { c = 0; ++j; }
-        }
-        uint8_t* dst = h + (int64_t)q * N + n4;
-        if (n4 + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 3u) == 0) *reinterpret_cast<uint32_t*>(dst) = word;
-        else for (int u = 0; n4 + u < N; ++u) dst[u] = (uint8_t)(word >> (8 * u));
-      }
-    }
-  }
-  if (a.post) {
-    for (int q = 0; q < ncw; ++q) {
-      const uint32_t cb = sbase + (uint32_t)q * cws;
-      for (int n = tid; n < N; n += nthr) {
-        const int j = n / Z, c = n - j * Z;
-        const auto v = A::lds(cb + c * RS + j * A::kElem);
-        if constexpr (A::kElem == 4) reinterpret_cast<float*>(a.post)[(cw0 + q) * N + n] = v;
-        else reinterpret_cast<int16_t*>(a.post)[(cw0 + q) * N + n] = (int16_t)v;
-      }
-    }
-  }
+  uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
+  float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
+  store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
+                       [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
+                       [](uint32_t v) { return __uint_as_float(v); });
   // ---- release TMEM ------------------------------------------------------------------
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
