@@ -14,7 +14,7 @@ ncu --set full --clock-control none --import-source on -k regex:decode_layered -
   python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/p_ncu_c2.log 2>&1
 python tools/profile_summary.py gpurun_out/prof_c2.ncu-rep C2 $OUT
 python bench.py --config C5 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/p_plain_c5.log 2>&1 || exit 1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"qcb" -c 400 --csv --log-file gpurun_out/launches_c5.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode|encode" -c 100 --csv --log-file gpurun_out/launches_c5.csv \
   python bench.py --config C5 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/p_ncu_list_c5.log 2>&1
 python tools/profile_summary.py --launches gpurun_out/launches_c5.csv C5 gpurun_out/r01_launches_c5.json
 ncu --set full --clock-control none --import-source on -k regex:decode_pair16 -s 1 -c 1 -o gpurun_out/prof_c5 -f \
