@@ -245,6 +245,31 @@ def test_empty_and_tiny_batches():
     assert out[0].shape == (0, h.n)
 
 
+@pytest.mark.parametrize("fixed", [False, True])
+def test_misaligned_device_buffers_take_the_scalar_paths(fixed):
+    """LLR / output tensors that are views at an element offset (not 16-byte
+    aligned) must give the same results as aligned ones (vectorised prologue /
+    epilogue fall back to element accesses)."""
+    mm = P.get_model_matrix("wimax", 2304, "1/2")
+    llr, _, _ = noisy_llrs(mm, 300, 1.8, seed=77, fixed=fixed)
+    cfg = P.DecoderConfig(max_iterations=6, early_termination=False,
+                          arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
+    dt = torch.int16 if fixed else torch.float32
+    aligned = torch.from_numpy(llr).cuda()
+    flat = torch.empty(llr.size + 1, dtype=dt, device="cuda")
+    flat[1:] = aligned.reshape(-1)
+    shifted = flat[1:].view(llr.shape)
+    assert shifted.data_ptr() % 16 != 0
+    ref = P.decode_batch(mm, aligned, cfg, posteriors=True)
+    hard_buf = torch.empty(300 * mm.n + 3, dtype=torch.uint8, device="cuda")
+    post_buf = torch.empty(llr.size + 1, dtype=dt, device="cuda")
+    out = (hard_buf[3:].view(300, mm.n), torch.empty(300, dtype=torch.int32, device="cuda"),
+           torch.empty(300, dtype=torch.uint8, device="cuda"), post_buf[1:].view(llr.shape))
+    got = P.decode_batch(mm, shifted, cfg, posteriors=True, out=out)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("config", ["C2", "C3"])
 def test_full_size_batch_properties(config):
     """BASELINE sizes: full batch on the GPU, a seeded sample checked against the
