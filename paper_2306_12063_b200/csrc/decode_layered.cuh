@@ -51,6 +51,27 @@ namespace qcb {
 constexpr int kLayMaxThreads = 384;
 constexpr int kLayMaxCw = 16;
 
+// Thread -> (codeword g, row r).  Rows are dealt out contiguously (lane l of
+// warp w: row 32w + l) except for one codeword per CTA with W = ceil(Z/32) odd
+// warps and W | Z (Wi-Fi Z = 81, WiMAX Z = 72, 84): then warp w takes rows
+// w, w+W, w+2W, ...  Every tier reads cells c = (r + e) mod Z, so a warp's
+// cells are then a whole residue class mod W, {y + W k}, whose 32-bank
+// residues W k mod 32 are distinct (W odd): no bank conflicts, where 32
+// consecutive rows wrapping at Z put up to two lanes on one bank.  Padding
+// lanes shadow a real lane of the same warp (same row, same words, lockstep).
+struct RowMap {
+  int g, r;
+};
+__device__ __forceinline__ RowMap map_row(int tid, int G, int Z) {
+  const int W = (Z + 31) >> 5;
+  if (G == 1 && W > 1 && (W & 1) && Z % W == 0) {
+    const int per = Z / W, lane = tid & 31;
+    return RowMap{0, (tid >> 5) + W * (lane < per ? lane : lane % per)};
+  }
+  const int twin = tid < G * Z ? tid : (tid & ~31) + ((tid & 31) % (G * Z - (tid & ~31)));
+  return RowMap{twin / Z, twin % Z};
+}
+
 // ---------------------------------------------------------------------------
 // small PTX helpers: multipliers come from the parameter block (constant bank)
 // so ptxas keeps them as IMAD (FMA-heavy pipe) instead of ALU shifts
@@ -589,8 +610,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   // conflict, identical values).  A separate scratch block costs a 2-way bank
   // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
   // shared-memory wavefronts).
-  const int twin = tid < G * Z ? tid : (tid & ~31) + ((tid & 31) % (G * Z - (tid & ~31)));
-  const int gs = twin / Z, rs = twin - gs * Z;
+  const RowMap rm = map_row(tid, G, Z);
+  const int gs = rm.g, rs = rm.r;
   const bool act = gs < ncw;
   // opaque copies keep the row bases in registers (no per-tier rematerialisation)
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;

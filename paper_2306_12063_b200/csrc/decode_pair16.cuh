@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   // conflict, identical values).  A separate scratch block costs a 2-way bank
   // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
   // shared-memory wavefronts).
-  const int twin = tid < G * Z ? tid : (tid & ~31) + ((tid & 31) % (G * Z - (tid & ~31)));
-  const int gs = twin / Z, rs = twin - gs * Z;
+  const RowMap rm = map_row(tid, G, Z);
+  const int gs = rm.g, rs = rm.r;
   const bool act = gs < npairs;
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
