@@ -171,7 +171,7 @@ def cpu_decode_rate(wl, seconds: float, threads: int):
         t0 = time.perf_counter()
         O.decode_batch(h, llr, wl.iters, False, workers=threads)
         dt = time.perf_counter() - t0
-        w2 = int(min(max(w, w * per_code / max(dt, 1e-6)), 1 << 17))
+        w2 = int(min(max(w, w * per_code / max(dt, 1e-6)), 1 << 18))
         w2 = max(threads, (w2 // threads) * threads)
         llr, _ = host_llrs(mm, w2, wl.ebn0_db, [wl.seed, ci, 100], wl.fixed)
         t0 = time.perf_counter()
