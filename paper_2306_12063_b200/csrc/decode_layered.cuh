@@ -254,13 +254,17 @@ __device__ __forceinline__ void tier_addrs(const SpecArgs& a, int r, uint32_t b0
 #define QCB_ADDR_TAB 1
 #endif
 // Measured per structure (tools/exp/percode.py, round 1, table vs selects):
-// float32 gains on WiMAX 2/3B, 3/4A, 3/4B (+7..11 %) and loses on every Wi-Fi
-// code and WiMAX 1/2 (-6..-22 %: those keep enough addresses hoisted in
-// registers); the int16 pair kernel gains on all WiMAX codes (+5..24 %) and
+// float32 gains on WiMAX 2/3B, 3/4A, 3/4B (+7..11 %) and Wi-Fi 1944 R2/3, R3/4
+// (+3 %, re-measured after the shadow-lane change) and loses elsewhere (up to
+// -11 %: those keep enough addresses hoisted in registers); the int16 pair kernel gains on all WiMAX codes (+5..24 %) and
 // Wi-Fi 1944 R2/3, R3/4 (+16 %), loses on Wi-Fi 648 R3/4, R5/6 and 1296 R5/6.
 template <class S, class A>
 constexpr bool use_addr_tab() {
-  constexpr unsigned kF32 = (1u << 14) | (1u << 15) | (1u << 16);
+#ifdef QCB_F32_TAB_MASK
+  constexpr unsigned kF32 = QCB_F32_TAB_MASK;   // tuning experiments
+#else
+  constexpr unsigned kF32 = (1u << 5) | (1u << 6) | (1u << 14) | (1u << 15) | (1u << 16);
+#endif
   constexpr unsigned kPair16 = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 6) | (1u << 8) | (1u << 9) |
                                (0x3Fu << 12);
   return QCB_ADDR_TAB && ((A::kKind == 0 && ((kF32 >> S::ID) & 1u)) || (A::kKind == 2 && ((kPair16 >> S::ID) & 1u)));
