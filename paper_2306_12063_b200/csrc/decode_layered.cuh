@@ -256,8 +256,9 @@ __device__ __forceinline__ void tier_addrs(const SpecArgs& a, int r, uint32_t b0
 // Measured per structure (tools/exp/percode.py, round 1, table vs selects):
 // float32 gains on WiMAX 2/3B, 3/4A, 3/4B (+7..11 %) and Wi-Fi 1944 R2/3, R3/4
 // (+3 %, re-measured after the shadow-lane change) and loses elsewhere (up to
-// -11 %: those keep enough addresses hoisted in registers); the int16 pair kernel gains on all WiMAX codes (+5..24 %) and
-// Wi-Fi 1944 R2/3, R3/4 (+16 %), loses on Wi-Fi 648 R3/4, R5/6 and 1296 R5/6.
+// -11 %: those keep enough addresses hoisted in registers); the int16 pair
+// kernel gains on all WiMAX codes (+5..24 %) and Wi-Fi 1944 R2/3, R3/4
+// (+16 %), loses on Wi-Fi 648 R3/4, R5/6 and 1296 R5/6.
 template <class S, class A>
 constexpr bool use_addr_tab() {
 #ifdef QCB_F32_TAB_MASK
