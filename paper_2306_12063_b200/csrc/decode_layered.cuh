@@ -655,6 +655,22 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
       __syncthreads();
     }
     if (tid < ncw) s_iters[tid] = a.max_iters;
+  } else if (G == 1) {
+    // one codeword per CTA: full sweeps, then the syndrome (_kernels.py:85-96)
+    // reduced with a single __syncthreads_or; stop at the first zero syndrome
+    // (the reference's break), iterations = sweeps done
+    int k = 0;
+    int fail = 1;
+    while (k < a.max_iters) {
+      L::template sweep<false>(a, K, rs, b0, b1, tab, mbase, msg, act, tiers);
+      ++k;
+      fail = __syncthreads_or(act && L::parity_all(a, rs, b0, b1, tab, tiers));
+      if (!fail) break;
+    }
+    if (tid == 0) {
+      s_iters[0] = k;
+      s_fail[0] = fail;
+    }
   } else {
     for (int k = 0; k < a.max_iters; ++k) {
       const bool work = act && !s_done[gs];

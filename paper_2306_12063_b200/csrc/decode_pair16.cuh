@@ -144,14 +144,13 @@ struct Layered2 {
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
     tier_addrs_tab<S, A, ZS, TAB, E0>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+    // hard = post <= 0 per lane: max(post, -32767) - 1 is negative exactly for
+    // post <= 0 (the max keeps -32768 from wrapping); XOR of the lane sign
+    // bits (15, 31) = the two codewords' row parities
     uint32_t par = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const uint32_t v = A::lds(addr[k]);
-      const int lo = sext16((int)v), hi = (int)v >> 16;           // hard = post <= 0 per lane
-      par ^= (lo <= 0 ? 1u : 0u) | (hi <= 0 ? 2u : 0u);
-    }
-    return par;
+    for (int k = 0; k < D; ++k) par ^= vadd2(vmax2(A::lds(addr[k]), 0x80018001u), 0xFFFFFFFFu);
+    return ((par >> 15) & 1u) | ((par >> 30) & 2u);
   }
 
   template <bool ET, int... Ts>
@@ -225,6 +224,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
   const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  // early-termination snapshot block (G == 1), after the address tables
+  const uint32_t snap_offset = ((uint32_t)G * cws + blockDim.x * (uint32_t)addr_tab_bytes_per_thread<S, ZS, L::TAB>() +
+                                15u) & ~15u;
   fill_addr_tab<S, ArithI16x2, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
@@ -255,6 +257,47 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       __syncthreads();
     }
     if (tid < ncw) s_iters[tid] = a.max_iters;
+  } else if (G == 1) {
+    // One pair per CTA.  Both lanes sweep unconditionally (no per-edge keep
+    // blending); when one lane converges while the other continues, its
+    // posteriors are saved to a snapshot block (that lane's halves only) and
+    // restored before the outputs -- exactly the reference's frozen codeword.
+    // The lanes' syndromes are reduced with __syncthreads_or.
+    const uint32_t snap = sbase + (uint32_t)snap_offset;
+    const int nwords = (int)(cws >> 2);
+    int k = 0, it_a = 0, it_b = 0;
+    int fail_a = 1, fail_b = 1;
+    bool done_a = false, done_b = ncw < 2;
+    uint32_t saved = 0;                                   // lane masks held in the snapshot
+    while (k < a.max_iters && !(done_a && done_b)) {
+      L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
+      ++k;
+      const uint32_t par = act ? L::parity_all(a, rs, b0, b1, tab, tiers) : 0u;
+      const int fa = __syncthreads_or((int)(par & 1u));
+      const int fb = __syncthreads_or((int)(par & 2u));
+      uint32_t newly = 0;
+      if (!done_a) { it_a = k; fail_a = fa; done_a = !fa; if (done_a) newly |= 0x0000FFFFu; }
+      if (!done_b) { it_b = k; fail_b = fb; done_b = !fb; if (done_b) newly |= 0xFFFF0000u; }
+      if (newly && !(done_a && done_b)) {                 // freeze: save the converged lane
+        for (int i = tid; i < nwords; i += blockDim.x) {
+          const uint32_t live = lds32(sbase + 4u * i), old = lds32(snap + 4u * i);
+          sts32(snap + 4u * i, (live & newly) | (old & ~newly));
+        }
+        saved |= newly;
+        __syncthreads();
+      }
+    }
+    if (saved) {                                          // restore the frozen lanes
+      for (int i = tid; i < nwords; i += blockDim.x) {
+        const uint32_t live = lds32(sbase + 4u * i), old = lds32(snap + 4u * i);
+        sts32(sbase + 4u * i, (old & saved) | (live & ~saved));
+      }
+    }
+    if (tid == 0) {
+      s_iters[0] = it_a; s_fail[0] = fail_a;
+      s_iters[1] = it_b; s_fail[1] = fail_b;
+    }
+    __syncthreads();
   } else {
     for (int k = 0; k < a.max_iters; ++k) {
       const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
@@ -302,8 +345,9 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)b.pairs * ((z * RS + 15) & ~15) +
-                      (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
+  const size_t cwsb = (size_t)((z * RS + 15) & ~15);
+  const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>() +
+                        15) & ~(size_t)15) + (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block
   e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   const int64_t per = 2 * (int64_t)b.pairs;
