@@ -154,3 +154,36 @@ def test_array_encoder_solves_parity_for_every_code():
         cw = P.encode_array(P.make_plan(mm), info)
         assert not P.row_parities(h, cw).any(), (std, n, rate)
         assert np.array_equal(cw[:, :mm.k], info)
+
+
+def test_channel_abi_validates_before_touching_the_device():
+    # argument checks run on the host and return before any CUDA call, so
+    # they are exercised here without a GPU (capi.cu qc_channel_llr ...).
+    L = _lib.lib()
+    buf = C.c_void_p(1)          # never dereferenced: every call fails first
+    cases = [
+        (L.qc_channel_llr, (buf, 4, 96, 0.0, None, 1, 0, 0, 0, 1.0, buf, None), "sigma2"),
+        (L.qc_channel_llr, (buf, 4, 95, 1.0, None, 1, 0, 0, 0, 1.0, buf, None), "bad shape"),
+        (L.qc_channel_llr, (buf, -1, 96, 1.0, None, 1, 0, 0, 0, 1.0, buf, None), "bad shape"),
+        (L.qc_channel_llr, (buf, 4, 96, 1.0, None, 1, 0, 0, 15, 1.0, buf, None), "q_b"),
+        (L.qc_channel_llr, (buf, 4, 96, 1.0, None, 1, 0, 0, 6, 0.0, buf, None), "l_clip"),
+        (L.qc_channel_llr, (None, 4, 96, 1.0, None, 1, 0, 0, 0, 1.0, buf, None), "NULL"),
+        (L.qc_quantize_llr, (buf, 8, 0, 1.0, buf, None), "q_b"),
+        (L.qc_quantize_llr, (buf, 8, 6, -1.0, buf, None), "l_clip"),
+        (L.qc_quantize_llr, (buf, -8, 6, 1.0, buf, None), "count"),
+        (L.qc_count_errors, (buf, 1, buf, buf, 4, 96, 97, 256, buf, None), "bad shape"),
+        (L.qc_count_errors, (buf, 1, buf, buf, 4, 96, 48, 0, buf, None), "bad shape"),
+        (L.qc_count_errors, (buf, 1, None, buf, 4, 96, 48, 256, buf, None), "NULL"),
+        (L.qc_pack_records, (buf, buf, buf, 4, 0, buf, None), "bad shape"),
+        (L.qc_pack_records, (buf, None, buf, 4, 96, buf, None), "NULL"),
+        (L.qc_frames_info, (1, 0, -1, 4, 48, buf, None), "negative"),
+        (L.qc_frames_info, (1, 0, 0, 4, 48, None, None), "NULL"),
+    ]
+    for fn, args, why in cases:
+        assert fn(*args) == _lib.QC_EINVAL, (fn.__name__, args)
+        assert why in L.qc_last_error().decode(), (fn.__name__, L.qc_last_error())
+    # empty work is a successful no-op
+    assert L.qc_channel_llr(None, 0, 96, 1.0, None, 1, 0, 0, 0, 1.0, None, None) == 0
+    assert L.qc_quantize_llr(None, 0, 6, 1.0, None, None) == 0
+    assert L.qc_pack_records(None, None, None, 0, 96, None, None) == 0
+    assert L.qc_frames_info(1, 0, 0, 0, 48, None, None) == 0
