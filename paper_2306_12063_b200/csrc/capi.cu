@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -262,7 +263,11 @@ int decode_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     }
   // chunked, double-buffered: H2D(i+1) overlaps decode(i) (two streams)
-  const int64_t chunk = std::min<int64_t>(w, std::max<int64_t>(2048, ((int64_t)64 << 20) / (n * (int64_t)sizeof(T))));
+  static const int64_t chunk_bytes = [] {
+    const char* v = getenv("QCB_HOST_CHUNK_MB");
+    return (int64_t)(v ? atoi(v) : 32) << 20;   // tools/exp/e2e_chunk.sh: 16-32 MB best
+  }();
+  const int64_t chunk = std::min<int64_t>(w, std::max<int64_t>(512, chunk_bytes / (n * (int64_t)sizeof(T))));
   const size_t llr_b = (size_t)chunk * n * sizeof(T), hard_b = (size_t)chunk * n;
   const size_t need = llr_b + hard_b + (size_t)chunk * 8 + 256;
   for (int i = 0; i < 2; ++i)
