@@ -110,6 +110,12 @@ int qc_decode_batch_i16_host(const int32_t* row_ptr, int64_t row_ptr_len, const 
  * info: w x K/8 bytes MSB-first; cw: w x N/8 bytes = [info | parity]. */
 int qc_encode_packed(qc_code_t code, const uint8_t* info, int64_t w, uint8_t* cw, void* cuda_stream);
 int qc_encode_packed_host(qc_code_t code, const uint8_t* info, int64_t w, uint8_t* cw);
+/* Bit-granular packed encoder for every Z <= 97: info = np.packbits of the
+ * K info bits (W x ceil(K/8) bytes), cw = np.packbits of the N codeword bits, i.e. exactly
+ * pack_bits(encode_array(...)) (encoder.py:103-104, 133-163) -- the layout the reference's
+ * packed encoder refuses for Z % 8 != 0 (encoder.py:59-61).  Byte-aligned Z: same as
+ * qc_encode_packed. */
+int qc_encode_bits(qc_code_t code, const uint8_t* info, int64_t w, uint8_t* cw, void* cuda_stream);
 
 /* ---- channel, waterfall counters and decode records -------
  * All pointers device memory, stream ordered.

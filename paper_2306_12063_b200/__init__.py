@@ -17,7 +17,7 @@ from .decoder import (Arithmetic, DecodeResult, DecoderConfig, DecoderState,
                       syndrome_check, tier_update)
 from .encoder import (EncoderPlan, EncoderVariant, bytes_to_words,
                       cyclic_shift_inverse, cyclic_shift_packed,
-                      default_word_bits, encode, encode_array, encode_packed,
+                      default_word_bits, encode, encode_array, encode_bits, encode_packed,
                       find_y, make_plan, pack_bits, unpack_bits, words_to_bytes)
 from .errors import (ArithmeticMismatch, BadZ, CodecError, CorruptFile,
                      DeviceError, DivByZeroSigma, MalformedHb,

@@ -48,6 +48,7 @@ SIGNATURES = {
     "qc_decode_batch_i16_host": (C.c_int, [P, i64, P, i64, i32, i32, P, i64, i64, i32, i32, P, P, P]),
     "qc_encode_packed": (C.c_int, [P, P, i64, P, P]),
     "qc_encode_packed_host": (C.c_int, [P, P, i64, P]),
+    "qc_encode_bits": (C.c_int, [P, P, i64, P, P]),
     "qc_encode_array": (C.c_int, [P, P, i64, P, P]),
     "qc_frames_info": (C.c_int, [C.c_uint64, C.c_uint32, i64, i64, i32, P, P]),
     "qc_channel_llr": (C.c_int, [P, i64, i32, C.c_double, P, C.c_uint64, C.c_uint32, i64, i32, C.c_double,

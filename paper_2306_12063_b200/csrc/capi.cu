@@ -420,6 +420,25 @@ int qc_encode_packed(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw, v
   return QC_OK;
 }
 
+int qc_encode_bits(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw, void* stream) {
+  if (!c) return fail(QC_EINVAL, "code is NULL");
+  if (c->z % 8 == 0) return qc_encode_packed(c, info, w, cw, stream);   // the same byte layout
+  if (c->enc_y < 0) return fail(QC_EMALFORMED, "h_b column lacks a single interior entry");
+  if (c->mb > 12 || c->nb > 24 || c->mb < 2 || c->z > 97)
+    return fail(QC_EUNSUPPORTED, "bit-granular encoder supports 2<=mb<=12, nb<=24, z<=97");
+  if (w < 0) return fail(QC_EINVAL, "w < 0");
+  if (w == 0) return QC_OK;
+  if (!info || !cw) return fail(QC_EINVAL, "NULL buffer");
+  EncodeArgs a;
+  memset(&a, 0, sizeof a);
+  a.info = info; a.cw = cw; a.w = w; a.mb = c->mb; a.nb = c->nb; a.z = c->z; a.hb_shift = c->enc_hb;
+  for (int i = 0; i < c->mb * c->nb; ++i) a.shifts[i] = c->shifts[i];
+  a.native = c->native ? 1 : 0;
+  cudaError_t e = launch_encode_packed(a, c->structure, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "encode_bits");
+  return QC_OK;
+}
+
 int qc_encode_packed_host(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw) {
   if (!c) return fail(QC_EINVAL, "code is NULL");
   if (w < 0) return fail(QC_EINVAL, "w < 0");

@@ -246,6 +246,52 @@ __device__ __forceinline__ void store_block(uint8_t* p, u128 v, int zb) {
 }
 __device__ __forceinline__ u128 z_mask(int z) { return z == 128 ? ~u128(0) : ((u128(1) << z) - 1); }
 
+// Bit-granular blocks (Z % 8 != 0): block j of a row is the
+// MSB-first bit field [j Z, (j + 1) Z) of the np.packbits byte row, read and
+// written through the row's big-endian 32-bit words (rows are 4-byte aligned;
+// the field plus its offset in the first word spans <= 4 words for Z <= 97).
+__device__ __forceinline__ u128 load_bits(const uint8_t* row, int off, int z) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (off >> 5);
+  const int sh = off & 31, nw = (sh + z + 31) >> 5;
+  u128 v = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nw) v = (v << 32) | bswap32(w[i]);
+  return (v >> (nw * 32 - sh - z)) & z_mask(z);
+}
+__device__ __forceinline__ void store_bits(uint8_t* row, int off, int z, u128 v) {   // replaces the field
+  uint32_t* w = reinterpret_cast<uint32_t*>(row) + (off >> 5);
+  const int sh = off & 31, nw = (sh + z + 31) >> 5, pad = nw * 32 - sh - z;
+  const u128 m = z_mask(z) << pad;
+  v = (v & z_mask(z)) << pad;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nw) {
+      const int s = (nw - 1 - i) * 32;
+      const uint32_t mi = (uint32_t)(m >> s), vi = (uint32_t)(v >> s);
+      w[i] = bswap32((bswap32(w[i]) & ~mi) | vi);
+    }
+}
+// the K info bits of a bit-granular row, copied word by word (+ a partial field)
+__device__ __forceinline__ void copy_info_bits(uint8_t* out, const uint8_t* u, int k) {
+  const int full = k >> 5;
+  for (int i = 0; i < full; ++i)
+    reinterpret_cast<uint32_t*>(out)[i] = reinterpret_cast<const uint32_t*>(u)[i];
+  if (k & 31) store_bits(out, full << 5, k & 31, load_bits(u, full << 5, k & 31));
+}
+// Block access for either layout: byte-aligned (BITS = false) or bit-granular.
+template <bool BITS>
+__device__ __forceinline__ u128 get_block(const uint8_t* row, int j, int z) {
+  if constexpr (BITS) return load_bits(row, j * z, z);
+  else return load_block(row + j * (z >> 3), z >> 3);
+}
+template <bool BITS>
+__device__ __forceinline__ void put_block(uint8_t* row, int j, int z, u128 v) {
+  if constexpr (BITS) store_bits(row, j * z, z, v);
+  else store_block(row + j * (z >> 3), v, z >> 3);
+}
+__host__ __device__ constexpr int bytes_of_bits(int bits) { return (bits + 7) >> 3; }
+
 template <class S, int T, int J>
 __device__ __forceinline__ void acc_rt(u128& s, const u128& uj, const EncodeArgs& a, u128 mask) {
   if constexpr (entry_at<S>(T, J) >= 0) s ^= rotl_z(uj, a.shifts[T * S::NB + J], a.z, mask);
@@ -255,16 +301,18 @@ __device__ __forceinline__ void col_rt(u128 (&s)[S::MB], const u128& uj, const E
                                        std::integer_sequence<int, Ts...>) {
   (acc_rt<S, Ts, J>(s[Ts], uj, a, mask), ...);
 }
-template <class S, int... Js>
-__device__ __forceinline__ void cols_rt(u128 (&s)[S::MB], const uint8_t* u, int zb, const EncodeArgs& a,
+template <class S, bool BITS, int... Js>
+__device__ __forceinline__ void cols_rt(u128 (&s)[S::MB], const uint8_t* u, int z, const EncodeArgs& a,
                                         u128 mask, std::integer_sequence<int, Js...>) {
-  (col_rt<S, Js>(s, load_block(u + Js * zb, zb), a, mask, std::make_integer_sequence<int, S::MB>{}), ...);
+  (col_rt<S, Js>(s, get_block<BITS>(u, Js, z), a, mask, std::make_integer_sequence<int, S::MB>{}), ...);
 }
 
-template <class S>
+// BITS: Z % 8 != 0, rows are np.packbits of K / N bits
+template <class S, bool BITS>
 __global__ void __launch_bounds__(kEncThreads) encode_struct_kernel(const __grid_constant__ EncodeArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int z = a.z, zb = z >> 3, kbytes = S::KB * zb, nbytes = S::NB * zb;
+  const int z = a.z, k = S::KB * z;
+  const int kbytes = bytes_of_bits(k), nbytes = bytes_of_bits(S::NB * z);
   const int in_stride = enc_stride(kbytes), out_stride = enc_stride(nbytes);
   uint8_t* sin = sm;
   uint8_t* sout = sm + kEncThreads * in_stride;
@@ -277,25 +325,30 @@ __global__ void __launch_bounds__(kEncThreads) encode_struct_kernel(const __grid
     if (threadIdx.x < ncw) {
       const uint8_t* u = sin + threadIdx.x * in_stride;
       uint8_t* out = sout + threadIdx.x * out_stride;
+      if constexpr (BITS) {
+        reinterpret_cast<uint32_t*>(out)[(nbytes - 1) >> 2] = 0;   // np.packbits pads with zeros
+        copy_info_bits(out, u, k);
+      }
       u128 s[S::MB];
 #pragma unroll
       for (int i = 0; i < S::MB; ++i) s[i] = 0;
-      cols_rt<S>(s, u, zb, a, mask, std::make_integer_sequence<int, S::KB>{});
+      cols_rt<S, BITS>(s, u, z, a, mask, std::make_integer_sequence<int, S::KB>{});
       u128 ssum = 0;
 #pragma unroll
       for (int i = 0; i < S::MB; ++i) ssum ^= s[i];
       const u128 v0 = rotl_z(ssum, (z - a.hb_shift) % z, z, mask);
-      store_block(out + kbytes, v0, zb);
+      put_block<BITS>(out, S::KB, z, v0);
       u128 v = s[0] ^ rotl_z(v0, (a.shifts[S::KB] % z + z) % z, z, mask);
-      store_block(out + kbytes + zb, v, zb);
+      put_block<BITS>(out, S::KB + 1, z, v);
 #pragma unroll
       for (int i = 1; i < S::MB - 1; ++i) {
         v ^= s[i];
         const int hb = a.shifts[i * S::NB + S::KB];
         if (hb >= 0) v ^= rotl_z(v0, hb, z, mask);
-        store_block(out + kbytes + (i + 1) * zb, v, zb);
+        put_block<BITS>(out, S::KB + i + 1, z, v);
       }
-      for (int b = 0; b < kbytes; ++b) out[b] = u[b];
+      if constexpr (!BITS)
+        for (int b = 0; b < kbytes; ++b) out[b] = u[b];
     }
     __syncthreads();
     stage_out(a.cw + cw0 * nbytes, sout, ncw, nbytes, out_stride);
@@ -303,10 +356,11 @@ __global__ void __launch_bounds__(kEncThreads) encode_struct_kernel(const __grid
   }
 }
 
+template <bool BITS>
 __global__ void __launch_bounds__(kEncThreads) encode_generic_kernel(const __grid_constant__ EncodeArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int z = a.z, mb = a.mb, nb = a.nb, kb = nb - mb;
-  const int zb = z >> 3, kbytes = kb * zb, nbytes = nb * zb;
+  const int kbytes = bytes_of_bits(kb * z), nbytes = bytes_of_bits(nb * z);
   const int in_stride = enc_stride(kbytes), out_stride = enc_stride(nbytes);
   uint8_t* sin = sm;
   uint8_t* sout = sm + kEncThreads * in_stride;
@@ -318,34 +372,213 @@ __global__ void __launch_bounds__(kEncThreads) encode_generic_kernel(const __gri
     __syncthreads();
     if (threadIdx.x < ncw) {
       const uint8_t* u = sin + threadIdx.x * in_stride;
-      uint8_t* out = sout + threadIdx.x * out_stride;
-      uint8_t* par = out + kbytes;                 // S_i accumulate in the output row
-      for (int i = 0; i < mb; ++i) store_block(par + i * zb, 0, zb);
+      uint8_t* out = sout + threadIdx.x * out_stride;   // S_i accumulate in the parity blocks
+      if constexpr (BITS) {
+        reinterpret_cast<uint32_t*>(out)[(nbytes - 1) >> 2] = 0;
+        copy_info_bits(out, u, kb * z);
+      }
+      for (int i = 0; i < mb; ++i) put_block<BITS>(out, kb + i, z, 0);
       for (int j = 0; j < kb; ++j) {
-        const u128 uj = load_block(u + j * zb, zb);
+        const u128 uj = get_block<BITS>(u, j, z);
         for (int i = 0; i < mb; ++i) {
           const int e = a.shifts[i * nb + j];
-          if (e >= 0) store_block(par + i * zb, load_block(par + i * zb, zb) ^ rotl_z(uj, e, z, mask), zb);
+          if (e >= 0) put_block<BITS>(out, kb + i, z, get_block<BITS>(out, kb + i, z) ^ rotl_z(uj, e, z, mask));
         }
       }
       u128 ssum = 0;
-      for (int i = 0; i < mb; ++i) ssum ^= load_block(par + i * zb, zb);
+      for (int i = 0; i < mb; ++i) ssum ^= get_block<BITS>(out, kb + i, z);
       const u128 v0 = rotl_z(ssum, (z - a.hb_shift) % z, z, mask);
-      const u128 s0 = load_block(par, zb);
-      store_block(par, v0, zb);
+      const u128 s0 = get_block<BITS>(out, kb, z);
+      put_block<BITS>(out, kb, z, v0);
       u128 v = s0 ^ rotl_z(v0, (a.shifts[kb] % z + z) % z, z, mask);
       for (int i = 1; i < mb - 1; ++i) {
-        const u128 si = load_block(par + i * zb, zb);
-        store_block(par + i * zb, v, zb);
+        const u128 si = get_block<BITS>(out, kb + i, z);
+        put_block<BITS>(out, kb + i, z, v);
         v ^= si;
         const int hb = a.shifts[i * nb + kb];
         if (hb >= 0) v ^= rotl_z(v0, hb, z, mask);
       }
-      store_block(par + (mb - 1) * zb, v, zb);
-      for (int b = 0; b < kbytes; ++b) out[b] = u[b];
+      put_block<BITS>(out, kb + mb - 1, z, v);
+      if constexpr (!BITS)
+        for (int b = 0; b < kbytes; ++b) out[b] = u[b];
     }
     __syncthreads();
     stage_out(a.cw + cw0 * nbytes, sout, ncw, nbytes, out_stride);
+    __syncthreads();
+  }
+}
+
+// ---- native Z % 8 != 0 (Wi-Fi Z0 = 27 / 54 / 81): compile-time shifts -------------
+// A Z-bit block is W = ceil(Z/32) big-endian words (bit 0 = MSB of word 0, pad
+// bits zero).  Thread c loads its np.packbits info row from a linear copy of the
+// tile into registers (one runtime funnel shift per word: the row starts at
+// bit 8 c ceil(K/8)); from there every block offset, rotation and output
+// position is a compile-time constant, so the XOR work is funnel shifts on
+// registers.  The codeword row is streamed into a linear output tile at its
+// own byte offset: interior words are plain stores, the two words shared with
+// the neighbouring rows are ORed in (atomicOr on the zeroed tile).
+template <int Z>
+struct BZ {
+  static constexpr int W = (Z + 31) / 32;
+  static constexpr uint32_t LAST = (Z % 32) ? ~0u << (32 - Z % 32) : ~0u;
+  uint32_t w[W];
+};
+template <int Z, int E>
+__device__ __forceinline__ BZ<Z> rotlz(const BZ<Z>& x) {   // out bit p = in bit (p + E) mod Z
+  if constexpr (E == 0) {
+    return x;
+  } else {
+    constexpr int W = BZ<Z>::W, la = E / 32, lr = E % 32, ra = (Z - E) / 32, rr = (Z - E) % 32;
+    auto get = [&](int i) { return (i >= 0 && i < W) ? x.w[i] : 0u; };
+    BZ<Z> o;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      const uint32_t l = lr == 0 ? get(q + la) : __funnelshift_l(get(q + la + 1), get(q + la), lr);
+      const uint32_t r = rr == 0 ? get(q - ra) : __funnelshift_r(get(q - ra), get(q - ra - 1), rr);
+      o.w[q] = l | r;
+    }
+    o.w[W - 1] &= BZ<Z>::LAST;
+    return o;
+  }
+}
+template <int Z>
+__device__ __forceinline__ void bz_xor(BZ<Z>& a, const BZ<Z>& b) {
+#pragma unroll
+  for (int q = 0; q < BZ<Z>::W; ++q) a.w[q] ^= b.w[q];
+}
+
+template <class S>
+struct ZBitsTile {
+  static constexpr int Z = S::Z0, K = S::KB * Z, N = S::NB * Z;
+  static constexpr int KBYTES = (K + 7) / 8, NBYTES = (N + 7) / 8;
+  static constexpr int KW = (K + 31) / 32, NW = (N + 31) / 32;   // row words (info / codeword)
+  static constexpr int K0 = K / 32;                               // codeword words holding only info bits
+  static constexpr int IN_BYTES = kEncThreads * KBYTES, OUT_BYTES = kEncThreads * NBYTES;
+  static constexpr int IN_ALLOC = (IN_BYTES + 16 + 15) & ~15, OUT_ALLOC = (OUT_BYTES + 16 + 15) & ~15;
+  static constexpr size_t SMEM = (size_t)IN_ALLOC + OUT_ALLOC;
+};
+
+template <class S, int Z, int KW, int OFF>
+__device__ __forceinline__ BZ<Z> block_of(const uint32_t (&R)[KW]) {   // bits [OFF, OFF + Z) of the row
+  constexpr int a = OFF / 32, r = OFF % 32;
+  auto get = [&](int i) { return i < KW ? R[i] : 0u; };
+  BZ<Z> x;
+#pragma unroll
+  for (int q = 0; q < BZ<Z>::W; ++q) x.w[q] = r == 0 ? get(a + q) : __funnelshift_l(get(a + q + 1), get(a + q), r);
+  x.w[BZ<Z>::W - 1] &= BZ<Z>::LAST;
+  return x;
+}
+template <class S, int Z, int KW, int T, int J>
+__device__ __forceinline__ void accz(BZ<Z>& s, const BZ<Z>& uj) {
+  constexpr int e = entry_at<S>(T, J);
+  if constexpr (e >= 0) bz_xor(s, rotlz<Z, S::SHIFT0[e]>(uj));
+}
+template <class S, int Z, int KW, int J, int... Ts>
+__device__ __forceinline__ void colz(BZ<Z> (&s)[S::MB], const BZ<Z>& uj, std::integer_sequence<int, Ts...>) {
+  (accz<S, Z, KW, Ts, J>(s[Ts], uj), ...);
+}
+template <class S, int Z, int KW, int... Js>
+__device__ __forceinline__ void colsz(BZ<Z> (&s)[S::MB], const uint32_t (&R)[KW], std::integer_sequence<int, Js...>) {
+  (colz<S, Z, KW, Js>(s, block_of<S, Z, KW, Js * Z>(R), std::make_integer_sequence<int, S::MB>{}), ...);
+}
+template <class S, int Z, int T>
+__device__ __forceinline__ void hbz(BZ<Z>& v, const BZ<Z>& v0) {
+  constexpr int e = entry_at<S>(T, S::KB);
+  if constexpr (e >= 0) bz_xor(v, rotlz<Z, S::SHIFT0[e]>(v0));
+}
+// OR block v into the codeword words O at row bit offset OFF
+template <int Z, int OFF, int NW>
+__device__ __forceinline__ void put_z(uint32_t (&O)[NW], const BZ<Z>& v) {
+  constexpr int wi = OFF / 32, sh = OFF % 32;
+#pragma unroll
+  for (int q = 0; q < BZ<Z>::W; ++q) {
+    if (wi + q < NW) O[wi + q] |= sh == 0 ? v.w[q] : v.w[q] >> sh;
+    if (sh != 0 && wi + q + 1 < NW) O[wi + q + 1] |= v.w[q] << (32 - sh);
+  }
+}
+template <class S, int Z, int T, int NW>
+__device__ __forceinline__ void chainz(BZ<Z>& v, const BZ<Z>& v0, const BZ<Z> (&s)[S::MB], uint32_t (&O)[NW]) {
+  if constexpr (T + 1 < S::MB) {                           // v_{T+1} = v_T ^ S_T ^ [hb_T] P v_0
+    bz_xor(v, s[T]);
+    hbz<S, Z, T>(v, v0);
+    put_z<Z, S::KB * Z + (T + 1) * Z>(O, v);
+    chainz<S, Z, T + 1>(v, v0, s, O);
+  }
+}
+
+template <class S>
+__global__ void __launch_bounds__(kEncThreads) encode_zbits_kernel(const __grid_constant__ EncodeArgs a) {
+  using T = ZBitsTile<S>;
+  constexpr int Z = T::Z;
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* lin = reinterpret_cast<uint32_t*>(sm);                  // the tile's info rows, contiguous
+  uint32_t* lout = reinterpret_cast<uint32_t*>(sm + T::IN_ALLOC);   // the tile's codeword rows, contiguous
+  const int tid = threadIdx.x;
+  const bool in_al = (reinterpret_cast<uintptr_t>(a.info) & 15) == 0;
+  const bool out_al = (reinterpret_cast<uintptr_t>(a.cw) & 15) == 0;
+  for (int64_t tile = blockIdx.x; tile * kEncThreads < a.w; tile += gridDim.x) {
+    const int64_t cw0 = tile * kEncThreads;
+    const int ncw = (int)(a.w - cw0 < kEncThreads ? a.w - cw0 : kEncThreads);
+    const bool full = ncw == kEncThreads;
+    const uint8_t* gin = a.info + cw0 * T::KBYTES;
+    if (in_al && full) {
+      const uint4* g = reinterpret_cast<const uint4*>(gin);
+      for (int i = tid; i < T::IN_BYTES / 16; i += kEncThreads) reinterpret_cast<uint4*>(lin)[i] = __ldcs(g + i);
+    } else {
+      for (int i = tid; i < ncw * T::KBYTES; i += kEncThreads) sm[i] = gin[i];
+    }
+    for (int i = tid; i < T::OUT_ALLOC / 16; i += kEncThreads) reinterpret_cast<uint4*>(lout)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (tid < ncw) {
+      // the info row as big-endian words
+      const uint32_t b0 = (uint32_t)tid * T::KBYTES, a0 = b0 >> 2, sh_in = 8 * (b0 & 3);
+      uint32_t R[T::KW];
+#pragma unroll
+      for (int m = 0; m < T::KW; ++m) R[m] = __funnelshift_l(bswap32(lin[a0 + m + 1]), bswap32(lin[a0 + m]), sh_in);
+      if constexpr (T::K % 32 != 0) R[T::KW - 1] &= ~0u << (32 - T::K % 32);
+      BZ<Z> s[S::MB];
+#pragma unroll
+      for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+        for (int q = 0; q < BZ<Z>::W; ++q) s[i].w[q] = 0;
+      colsz<S, Z, T::KW>(s, R, std::make_integer_sequence<int, S::KB>{});
+      BZ<Z> ssum = s[0];
+#pragma unroll
+      for (int i = 1; i < S::MB; ++i) bz_xor(ssum, s[i]);
+      uint32_t O[T::NW];
+#pragma unroll
+      for (int m = 0; m < T::NW; ++m) O[m] = m < T::KW ? R[m] : 0u;   // systematic bits
+      const BZ<Z> v0 = rotlz<Z, (Z - hb_y_shift<S>()) % Z>(ssum);
+      put_z<Z, T::K>(O, v0);
+      BZ<Z> v = s[0];
+      hbz<S, Z, 0>(v, v0);
+      put_z<Z, T::K + Z>(O, v);
+      chainz<S, Z, 1>(v, v0, s, O);
+      // stream the row into the linear tile at bit offset 8 c NBYTES
+      const uint32_t ob = (uint32_t)tid * T::NBYTES, w0 = ob >> 2, sh = 8 * (ob & 3);
+      constexpr int LAST_T = T::NW;                          // words t = 0 .. NW touched when sh != 0
+#pragma unroll
+      for (int t = 0; t <= LAST_T; ++t) {
+        const uint32_t hi = t > 0 ? O[t - 1] : 0u, lo = t < T::NW ? O[t] : 0u;
+        const uint32_t y = bswap32(__funnelshift_r(lo, hi, sh));
+        // first / last words may hold a neighbour's bytes: OR them in
+        const bool edge = t == 0 || t >= (int)((sh + 8 * T::NBYTES) >> 5);
+        if (edge) {
+          if (y) atomicOr(lout + w0 + t, y);
+        } else {
+          lout[w0 + t] = y;
+        }
+      }
+    }
+    __syncthreads();
+    uint8_t* gout = a.cw + cw0 * T::NBYTES;
+    if (out_al && full) {
+      uint4* g = reinterpret_cast<uint4*>(gout);
+      for (int i = tid; i < T::OUT_BYTES / 16; i += kEncThreads) __stcs(g + i, reinterpret_cast<const uint4*>(lout)[i]);
+    } else {
+      const uint8_t* lb = reinterpret_cast<const uint8_t*>(lout);
+      for (int i = tid; i < ncw * T::NBYTES; i += kEncThreads) gout[i] = lb[i];
+    }
     __syncthreads();
   }
 }
@@ -363,7 +596,7 @@ static int64_t enc_grid(const void* kern, size_t smem, int64_t tiles, cudaError_
 
 template <class K>
 static cudaError_t launch_enc(K kern, const EncodeArgs& a, cudaStream_t s) {
-  const int zb = a.z >> 3, kbytes = (a.nb - a.mb) * zb, nbytes = a.nb * zb;
+  const int kbytes = bytes_of_bits((a.nb - a.mb) * a.z), nbytes = bytes_of_bits(a.nb * a.z);
   const size_t smem = (size_t)kEncThreads * (enc_stride(kbytes) + enc_stride(nbytes));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -396,21 +629,38 @@ static cudaError_t launch_z96(const EncodeArgs& a, cudaStream_t s) {
   r.info = a.info + full * (T::KW * 4);
   r.cw = a.cw + full * (T::NW * 4);
   r.w = a.w - full;
-  return launch_enc(encode_struct_kernel<S>, r, s);
+  return launch_enc(encode_struct_kernel<S, false>, r, s);
+}
+
+template <class S>
+static cudaError_t launch_zbits(const EncodeArgs& a, cudaStream_t s) {
+  using T = ZBitsTile<S>;
+  cudaError_t e = cudaFuncSetAttribute(encode_zbits_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)T::SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = enc_grid((const void*)encode_zbits_kernel<S>, T::SMEM, (a.w + kEncThreads - 1) / kEncThreads, &e);
+  if (e != cudaSuccess) return e;
+  encode_zbits_kernel<S><<<(unsigned)grid, kEncThreads, T::SMEM, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_encode_packed(const EncodeArgs& a, int structure_id, cudaStream_t s) {
   if (a.w <= 0) return cudaSuccess;
   if (a.mb < 2) return cudaErrorInvalidValue;
-#define QCB_ENC(STRUCT)                                                         \
-  if (structure_id == STRUCT::ID && STRUCT::NB == a.nb && STRUCT::MB == a.mb) { \
-    if constexpr (STRUCT::Z0 == 96)                                             \
-      if (a.native && a.z == 96) return launch_z96<STRUCT>(a, s);               \
-    return launch_enc(encode_struct_kernel<STRUCT>, a, s);                      \
+  const bool bits = (a.z & 7) != 0;
+  if (bits && a.z > 97) return cudaErrorInvalidValue;
+#define QCB_ENC(STRUCT)                                                                    \
+  if (structure_id == STRUCT::ID && STRUCT::NB == a.nb && STRUCT::MB == a.mb) {            \
+    if constexpr (STRUCT::Z0 == 96)                                                        \
+      if (a.native && a.z == 96) return launch_z96<STRUCT>(a, s);                          \
+    if constexpr (STRUCT::Z0 % 8 != 0)                                                     \
+      if (a.native && a.z == STRUCT::Z0) return launch_zbits<STRUCT>(a, s);                \
+    return bits ? launch_enc(encode_struct_kernel<STRUCT, true>, a, s)                     \
+                : launch_enc(encode_struct_kernel<STRUCT, false>, a, s);                   \
   }
   QCB_FOR_EACH_STRUCTURE(QCB_ENC)
 #undef QCB_ENC
-  return launch_enc(encode_generic_kernel, a, s);
+  return bits ? launch_enc(encode_generic_kernel<true>, a, s) : launch_enc(encode_generic_kernel<false>, a, s);
 }
 
 }  // namespace qcb

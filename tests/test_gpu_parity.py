@@ -370,3 +370,43 @@ def test_encode_then_decode_round_trip_c5_scale():
     hard, it, conv = P.decode_batch(mm, llr, cfg, hard_packed=True)
     assert bool(conv.all()) and bool((it == 1).all())
     assert torch.equal(hard, cw[:65536])
+
+
+def test_bit_granular_encoder_all_codes_any_z():
+    """np.packbits-layout encoding for every code, Z % 8 != 0
+    included (Wi-Fi Z = 27/54/81, scaled WiMAX Z = 28, 36, ...), equal to
+    pack_bits(encode_array) -- the reference's array encoder, encoder.py:133-163."""
+    rng = np.random.default_rng(2024)
+    n_unaligned = 0
+    for std, n, rate in P.supported_codes():
+        mm = P.get_model_matrix(std, n, rate)
+        n_unaligned += mm.z % 8 != 0
+        for w in (1, 129):
+            info = rng.integers(0, 2, size=(w, mm.k), dtype=np.uint8)
+            want = P.pack_bits(P.encode_array(P.make_plan(mm), info))
+            got = P.encode_bits(mm, P.pack_bits(info))
+            assert np.array_equal(got, want), (std, n, rate, w)
+    assert n_unaligned == 12 + 54
+
+
+def test_bit_granular_encoder_codewords_satisfy_h():
+    """Independent of encode_array: every encoded word is in the null space
+    of the expanded H (codebook.expand), for unaligned Z (structure kernels)
+    and a non-standard table (generic kernel), from a misaligned view."""
+    rng = np.random.default_rng(99)
+    base = P.get_model_matrix("wifi", 648, "1/2")
+    ent = base.entries.copy()
+    ent[0, 0] = -1                                     # not a standard zero pattern: generic kernel
+    generic = P.ModelMatrix(base.standard, base.rate, base.z, base.nb, base.kb, ent)
+    mms = [P.get_model_matrix("wifi", 648, "5/6"), P.get_model_matrix("wifi", 1944, "1/2"),
+           P.get_model_matrix("wimax", 672, "3/4A"), generic]
+    for mm in mms:
+        info = rng.integers(0, 2, size=(300, mm.k), dtype=np.uint8)
+        dev = torch.from_numpy(P.pack_bits(info)).cuda()
+        cw = P.unpack_bits(P.encode_bits(mm, dev[1:]).cpu().numpy(), mm.n)   # misaligned view
+        assert np.array_equal(cw[:, :mm.k], info[1:])
+        h = P.codebook.expand(mm)
+        rows = np.repeat(np.arange(h.m), np.diff(h.row_ptr))
+        syn = np.zeros((cw.shape[0], h.m), np.uint8)
+        np.bitwise_xor.at(syn.T, rows, cw[:, h.row_cols].T)
+        assert not syn.any(), (mm.n, mm.z)

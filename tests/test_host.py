@@ -178,6 +178,7 @@ def test_channel_abi_validates_before_touching_the_device():
         (L.qc_pack_records, (buf, None, buf, 4, 96, buf, None), "NULL"),
         (L.qc_frames_info, (1, 0, -1, 4, 48, buf, None), "negative"),
         (L.qc_frames_info, (1, 0, 0, 4, 48, None, None), "NULL"),
+        (L.qc_encode_bits, (None, buf, 4, buf, None), "NULL"),
     ]
     for fn, args, why in cases:
         assert fn(*args) == _lib.QC_EINVAL, (fn.__name__, args)
