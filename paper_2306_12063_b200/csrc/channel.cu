@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_cache.h"
 
 namespace qcb {
 
@@ -215,9 +216,7 @@ __global__ void pack_records_kernel(const uint8_t* hard_packed, const int32_t* i
 
 // ---- launchers -------------------------------------------------------------------
 static unsigned grid_for(int64_t items, int threads) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   const int64_t want = (items + threads - 1) / threads, cap = (int64_t)sms * 16;
   return (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
 }
@@ -233,12 +232,10 @@ cudaError_t launch_encode_array(const EncodeArgs& a, cudaStream_t s) {
   if (a.w <= 0) return cudaSuccess;
   const int k = (a.nb - a.mb) * a.z;
   const size_t smem = (size_t)k + (size_t)a.mb * a.z + a.z;
-  cudaError_t e = cudaFuncSetAttribute(encode_array_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dyn_smem((const void*)encode_array_kernel, smem);
   if (e != cudaSuccess) return e;
   const int threads = a.z >= 256 ? 256 : (a.z + 31) / 32 * 32;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   const int64_t grid = a.w < (int64_t)sms * 32 ? a.w : (int64_t)sms * 32;
   encode_array_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
   return cudaGetLastError();
@@ -269,9 +266,7 @@ cudaError_t launch_count_errors(const uint8_t* hard, int32_t packed, const uint8
   const int64_t nbatch = (w + batch - 1) / batch;
   cudaError_t e = cudaMemsetAsync(sums, 0, (size_t)nbatch * 3 * sizeof(unsigned long long), s);
   if (e != cudaSuccess || w <= 0) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sm_count();
   const int64_t grid = w < (int64_t)sms * 16 ? w : (int64_t)sms * 16;
   count_errors_kernel<<<(unsigned)grid, 128, 0, s>>>(hard, packed, info, iters, w, n, k, batch, sums);
   return cudaGetLastError();

@@ -28,6 +28,7 @@
 #include "bulk_copy.cuh"
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_cache.h"
 
 namespace qcb {
 
@@ -584,13 +585,11 @@ __global__ void __launch_bounds__(kEncThreads) encode_zbits_kernel(const __grid_
 }
 
 static int64_t enc_grid(const void* kern, size_t smem, int64_t tiles, cudaError_t* err) {
-  int dev = 0, sms = 148, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
-  if (*err != cudaSuccess) return 0;
+  int per_sm = 0;
+  if ((*err = ensure_dyn_smem(kern, smem)) != cudaSuccess) return 0;
+  if ((*err = kernel_occupancy(kern, kEncThreads, smem, &per_sm)) != cudaSuccess) return 0;
   if (per_sm < 1) { *err = cudaErrorLaunchOutOfResources; return 0; }
-  const int64_t cap = (int64_t)sms * per_sm;
+  const int64_t cap = (int64_t)device_sm_count() * per_sm;
   return tiles < cap ? tiles : cap;
 }
 
@@ -598,8 +597,7 @@ template <class K>
 static cudaError_t launch_enc(K kern, const EncodeArgs& a, cudaStream_t s) {
   const int kbytes = bytes_of_bits((a.nb - a.mb) * a.z), nbytes = bytes_of_bits(a.nb * a.z);
   const size_t smem = (size_t)kEncThreads * (enc_stride(kbytes) + enc_stride(nbytes));
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   const int64_t grid = enc_grid((const void*)kern, smem, (a.w + kEncThreads - 1) / kEncThreads, &e);
   if (e != cudaSuccess) return e;
   kern<<<(unsigned)grid, kEncThreads, smem, s>>>(a);
@@ -614,9 +612,7 @@ static cudaError_t launch_z96(const EncodeArgs& a, cudaStream_t s) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.info) | reinterpret_cast<uintptr_t>(a.cw)) & 15) == 0;
   const int64_t full = aligned ? a.w / kEncThreads * kEncThreads : 0;
   if (full > 0) {
-    cudaError_t e = cudaFuncSetAttribute(encode_z96_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)T::SMEM);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
     const int64_t grid = enc_grid((const void*)encode_z96_kernel<S>, T::SMEM, full / kEncThreads, &e);
     if (e != cudaSuccess) return e;
     EncodeArgs b = a;
@@ -635,9 +631,7 @@ static cudaError_t launch_z96(const EncodeArgs& a, cudaStream_t s) {
 template <class S>
 static cudaError_t launch_zbits(const EncodeArgs& a, cudaStream_t s) {
   using T = ZBitsTile<S>;
-  cudaError_t e = cudaFuncSetAttribute(encode_zbits_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)T::SMEM);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   const int64_t grid = enc_grid((const void*)encode_zbits_kernel<S>, T::SMEM, (a.w + kEncThreads - 1) / kEncThreads, &e);
   if (e != cudaSuccess) return e;
   encode_zbits_kernel<S><<<(unsigned)grid, kEncThreads, T::SMEM, s>>>(a);
