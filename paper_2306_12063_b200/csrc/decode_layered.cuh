@@ -46,6 +46,14 @@
 #include "kernels.h"
 #include "launch_cache.h"
 
+// early-termination syndrome with early exit (measured: tools/exp/ab_et.sh)
+#ifndef QCB_ET_EARLY_EXIT
+#define QCB_ET_EARLY_EXIT 1
+#endif
+#ifndef QCB_ET_CHUNKS
+#define QCB_ET_CHUNKS 2
+#endif
+
 namespace qcb {
 
 constexpr int kLayMaxThreads = 384;
@@ -549,6 +557,71 @@ struct Layered {
                                                         uint32_t tab, std::integer_sequence<int, Ts...>) {
     return (parity<Ts>(a, r, b0, b1, tab) | ...);
   }
+
+  // Early-termination syndrome with early exit: the CTA only needs the OR of
+  // all row parities, so the tiers are checked in QCB_ET_CHUNKS groups; a
+  // thread stops after the first group holding an odd row and publishes it in
+  // `flag`, the others stop at their next group once they see the flag.  (A
+  // poll per tier serialises the tiers' loads: measured slower at 3 iterations.)
+  // Returns 1 if this thread saw an odd row or the flag (the OR is 1 either way).
+  static constexpr int kEtChunk = QCB_ET_CHUNKS > 0 ? (S::MB + QCB_ET_CHUNKS - 1) / QCB_ET_CHUNKS : 1;
+  template <int T0, int... Is>
+  __device__ __forceinline__ static uint32_t parity_group(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                          uint32_t tab, std::integer_sequence<int, Is...>) {
+    return ((T0 + Is < S::MB ? parity<(T0 + Is < S::MB ? T0 + Is : 0)>(a, r, b0, b1, tab) : 0u) | ...);
+  }
+  // QCB_ET_CHUNKS == 0: per tier, software-pipelined -- tier T+1's loads and
+  // the flag poll are issued before tier T's parity is tested, so the early
+  // exit does not serialise the loads.
+  template <int T>
+  __device__ __forceinline__ static void parity_load(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab,
+                                                     Val (&v)[S::DEG[T]]) {
+    constexpr int D = S::DEG[T];
+    uint32_t addr[D];
+    tier_addrs_tab<S, A, ZS, TAB, S::START[T]>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = A::lds(addr[k]);
+  }
+  template <int T>
+  __device__ __forceinline__ static uint32_t parity_pipe(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                         uint32_t tab, volatile int* flag, const Val (&cur)[S::DEG[T]],
+                                                         int f_prev) {
+    constexpr int D = S::DEG[T];
+    uint32_t par = 0;
+    if constexpr (T + 1 < S::MB) {
+      Val nxt[S::DEG[T + 1]];
+      parity_load<T + 1>(a, r, b0, b1, tab, nxt);
+      const int f = *flag;
+#pragma unroll
+      for (int k = 0; k < D; ++k) par ^= A::hard(cur[k]) ? 1u : 0u;
+      if (par) { *flag = 1; return 1u; }
+      if (f_prev) return 1u;
+      return parity_pipe<T + 1>(a, r, b0, b1, tab, flag, nxt, f);
+    } else {
+#pragma unroll
+      for (int k = 0; k < D; ++k) par ^= A::hard(cur[k]) ? 1u : 0u;
+      return par | (f_prev ? 1u : 0u);
+    }
+  }
+  template <int T0>
+  __device__ __forceinline__ static uint32_t parity_any(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                        uint32_t tab, volatile int* flag) {
+#if QCB_ET_CHUNKS == 0
+    Val v0[S::DEG[0]];
+    parity_load<0>(a, r, b0, b1, tab, v0);
+    return parity_pipe<0>(a, r, b0, b1, tab, flag, v0, 0);
+#endif
+    if constexpr (T0 >= S::MB) {
+      return 0u;
+    } else {
+      if (*flag) return 1u;
+      if (parity_group<T0>(a, r, b0, b1, tab, std::make_integer_sequence<int, kEtChunk>{})) {
+        *flag = 1;
+        return 1u;
+      }
+      return parity_any<T0 + kEtChunk>(a, r, b0, b1, tab, flag);
+    }
+  }
 };
 
 // CTA shape.  A CTA holds p codewords (p*Z threads, padded to whole warps).
@@ -615,6 +688,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[kLayMaxCw], s_done[kLayMaxCw], s_iters[kLayMaxCw];
   __shared__ int s_active;
+  __shared__ int s_odd;                         // early-exit syndrome flag (G == 1 with ET)
 
   const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
@@ -654,6 +728,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
+    if (tid == 0) s_odd = 0;
   }
   __syncthreads();
 
@@ -681,7 +756,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
     while (k < a.max_iters) {
       L::template sweep<false>(a, K, rs, b0, b1, tab, mbase, msg, act, tiers);
       ++k;
+#if QCB_ET_EARLY_EXIT
+      fail = __syncthreads_or(act && L::template parity_any<0>(a, rs, b0, b1, tab, &s_odd));
+      if (tid == 0) s_odd = 0;                  // read again only after the next sweep's barriers
+#else
       fail = __syncthreads_or(act && L::parity_all(a, rs, b0, b1, tab, tiers));
+#endif
       if (!fail) break;
     }
     if (tid == 0) {

@@ -178,6 +178,70 @@ struct Layered2 {
                                                         uint32_t tab, std::integer_sequence<int, Ts...>) {
     return (parity<Ts>(a, r, b0, b1, tab) | ...);
   }
+
+  // Early-exit syndrome in QCB_ET_CHUNKS groups of tiers (see
+  // Layered::parity_any): lane bits found odd are ORed into `flag`; a thread
+  // stops once every lane in `need` is known to fail.  Returns this thread's
+  // bits | the flag's (a set flag bit means some thread found that lane odd).
+  static constexpr int kEtChunk = QCB_ET_CHUNKS > 0 ? (S::MB + QCB_ET_CHUNKS - 1) / QCB_ET_CHUNKS : 1;
+  template <int T0, int... Is>
+  __device__ __forceinline__ static uint32_t parity_group(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                          uint32_t tab, std::integer_sequence<int, Is...>) {
+    return ((T0 + Is < S::MB ? parity<(T0 + Is < S::MB ? T0 + Is : 0)>(a, r, b0, b1, tab) : 0u) | ...);
+  }
+  // QCB_ET_CHUNKS == 0: per tier, software-pipelined (see Layered::parity_pipe)
+  template <int T>
+  __device__ __forceinline__ static void parity_load(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab,
+                                                     uint32_t (&v)[S::DEG[T]]) {
+    constexpr int D = S::DEG[T];
+    uint32_t addr[D];
+    tier_addrs_tab<S, A, ZS, TAB, S::START[T]>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = A::lds(addr[k]);
+  }
+  template <int T>
+  __device__ __forceinline__ static uint32_t lane_parity(const uint32_t (&v)[S::DEG[T]]) {
+    constexpr int D = S::DEG[T];
+    uint32_t par = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) par ^= vadd2(vmax2(v[k], 0x80018001u), 0xFFFFFFFFu);
+    return ((par >> 15) & 1u) | ((par >> 30) & 2u);
+  }
+  template <int T>
+  __device__ __forceinline__ static uint32_t parity_pipe(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                         uint32_t tab, volatile int* flag, uint32_t need, uint32_t acc,
+                                                         const uint32_t (&cur)[S::DEG[T]], uint32_t f_prev) {
+    if constexpr (T + 1 < S::MB) {
+      uint32_t nxt[S::DEG[T + 1]];
+      parity_load<T + 1>(a, r, b0, b1, tab, nxt);
+      const uint32_t f = (uint32_t)*flag;
+      const uint32_t p = lane_parity<T>(cur) & need;
+      if (p & ~acc) atomicOr((int*)flag, (int)p);
+      acc |= p;
+      if (((acc | f_prev) & need) == need) return acc | (f_prev & need);
+      return parity_pipe<T + 1>(a, r, b0, b1, tab, flag, need, acc, nxt, f);
+    } else {
+      return acc | (lane_parity<T>(cur) & need) | (f_prev & need);
+    }
+  }
+  template <int T0>
+  __device__ __forceinline__ static uint32_t parity_any(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
+                                                        uint32_t tab, volatile int* flag, uint32_t need,
+                                                        uint32_t acc = 0) {
+#if QCB_ET_CHUNKS == 0
+    uint32_t v0[S::DEG[0]];
+    parity_load<0>(a, r, b0, b1, tab, v0);
+    return parity_pipe<0>(a, r, b0, b1, tab, flag, need, 0u, v0, 0u);
+#endif
+    if constexpr (T0 >= S::MB) {
+      return acc;
+    } else {
+      if (((acc | (uint32_t)*flag) & need) == need) return acc | ((uint32_t)*flag & need);
+      const uint32_t p = parity_group<T0>(a, r, b0, b1, tab, std::make_integer_sequence<int, kEtChunk>{}) & need;
+      if (p & ~acc) atomicOr((int*)flag, (int)p);
+      return parity_any<T0 + kEtChunk>(a, r, b0, b1, tab, flag, need, acc | p);
+    }
+  }
 };
 
 #ifndef QCB_P16_SLACK
@@ -199,6 +263,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
   __shared__ int s_active;
+  __shared__ int s_odd;                         // early-exit syndrome lane bits (G == 1 with ET)
 
   const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
@@ -235,6 +300,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
+    if (tid == 0) s_odd = 0;
   }
   __syncthreads();
 
@@ -272,9 +338,15 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     while (k < a.max_iters && !(done_a && done_b)) {
       L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
       ++k;
+#if QCB_ET_EARLY_EXIT
+      const uint32_t need = (done_a ? 0u : 1u) | (done_b ? 0u : 2u);
+      const uint32_t par = act ? L::template parity_any<0>(a, rs, b0, b1, tab, &s_odd, need) : 0u;
+#else
       const uint32_t par = act ? L::parity_all(a, rs, b0, b1, tab, tiers) : 0u;
+#endif
       const int fa = __syncthreads_or((int)(par & 1u));
       const int fb = __syncthreads_or((int)(par & 2u));
+      if (tid == 0) s_odd = 0;
       uint32_t newly = 0;
       if (!done_a) { it_a = k; fail_a = fa; done_a = !fa; if (done_a) newly |= 0x0000FFFFu; }
       if (!done_b) { it_b = k; fail_b = fb; done_b = !fb; if (done_b) newly |= 0xFFFF0000u; }
