@@ -136,3 +136,53 @@ def test_throughput_bench_report():
     rep = CH.run_throughput_bench(mm, P.DecoderConfig(), frames=4096)
     assert rep.frames == 4096 and rep.info_bits == 4096 * mm.k and rep.mbps > 0
     assert rep.csv_line().startswith("float32,1,cuda,4096,")
+
+
+def _crossing_db(points, target=1e-4):
+    """Eb/N0 where a BER curve crosses `target`, log-linear between points."""
+    pts = sorted(points)
+    for (x0, b0), (x1, b1) in zip(pts, pts[1:]):
+        if b0 >= target >= b1 > 0.0:
+            return x0 if b0 == b1 else x0 + math.log(b0 / target) / math.log(b0 / b1) * (x1 - x0)
+    raise AssertionError(f"target BER {target} not bracketed by {pts}")
+
+
+def test_fixed_point_penalty_within_budget():
+    """The reference's fixed-point pin (test_acceptance.py:182-205) on device
+    frames: int16 decoding crosses BER 1e-4 at most 0.15 dB (Wi-Fi 1944 R1/2)
+    / 0.05 dB (WiMAX 576 R5/6) right of float32, same noise for both."""
+    cases = [(("wifi", 1944, "1/2"), [2.1, 2.25, 2.4], 400, 20000, 0.15),
+             (("wimax", 576, "5/6"), [4.0, 4.25, 4.5], 350, 25000, 0.05)]
+    for code, snrs, min_err, max_frames, budget in cases:
+        mm = P.get_model_matrix(*code)
+        cross = {}
+        for arith in (P.Arithmetic.Float32, P.Arithmetic.Fixed16):
+            table = CH.run_waterfall(mm, P.DecoderConfig(arithmetic=arith), snrs, min_errors=min_err,
+                                     max_frames=max_frames, seed=1006)
+            cross[arith] = _crossing_db([(p.ebn0_db, p.ber) for p in table.points])
+        penalty = cross[P.Arithmetic.Fixed16] - cross[P.Arithmetic.Float32]
+        assert penalty <= budget, (code, penalty)
+
+
+def test_rate_curves_keep_order():
+    """test_acceptance.py:208-241 on device frames: with >= 1e4 bit errors per
+    point a lower rate never shows a higher BER at the same Eb/N0 and every
+    curve is monotone (Wi-Fi 1944, four rates)."""
+    plans = [("1/2", [2.3], 400_000), ("2/3", [2.3, 2.7], 60_000),
+             ("3/4", [2.3, 2.7, 3.1], 60_000), ("5/6", [2.3, 2.7, 3.1], 60_000)]
+    curves = {}
+    for rate, snrs, max_frames in plans:
+        mm = P.get_model_matrix("wifi", 1944, rate)
+        table = CH.run_waterfall(mm, P.DecoderConfig(), snrs, min_errors=10000, max_frames=max_frames, seed=1007)
+        for p in table.points:
+            assert p.bit_errors >= 10000, (rate, p)
+        curves[mm.rate.fraction] = {p.ebn0_db: p.ber for p in table.points}
+    comparisons = 0
+    for snr in (2.3, 2.7, 3.1):
+        ladder = sorted((frac, bers[snr]) for frac, bers in curves.items() if snr in bers)
+        for (_, b_lo), (_, b_hi) in zip(ladder, ladder[1:]):
+            comparisons += 1
+            assert b_lo <= b_hi, (snr, ladder)
+    assert comparisons == 6
+    for bers in curves.values():
+        assert (np.diff([bers[s] for s in sorted(bers)]) <= 0).all(), bers
