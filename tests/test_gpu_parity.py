@@ -172,6 +172,10 @@ def test_standard_structure_with_foreign_shifts():
             plan = P.make_plan(mm, P.EncoderVariant.Packed)
             dev = P.encode_packed(plan, torch.from_numpy(info).cuda()).cpu().numpy()
             assert np.array_equal(dev, O.encode_packed(mm, info)), (std, n, rate)
+        else:                                      # bit-granular encoder: runtime-shift kernel
+            bits = rng.integers(0, 2, size=(300, mm.k), dtype=np.uint8)
+            got = P.encode_bits(mm, P.pack_bits(bits))
+            assert np.array_equal(got, P.pack_bits(P.encode_array(P.make_plan(mm), bits))), (std, n, rate)
 
 
 def test_known_answers(golden_dir):
@@ -214,6 +218,20 @@ def test_sign_gauge_symmetry(fixed):
     for x, got in ((llr, a), (flip, b)):
         want = O.decode_batch(h, x, 10, True)
         assert all(np.array_equal(u, v) for u, v in zip(got, want))
+
+
+def test_float32_power_of_two_scale_invariance():
+    """Scaling float32 LLRs by a power of two changes no decision or
+    iteration count (reference test_decoder.py:166-176: WiMAX 576 R5/6,
+    3.5 dB, scales 1/4 and 4), plus a larger batch on the device."""
+    mm = P.get_model_matrix("wimax", 576, "5/6")
+    cfg = P.DecoderConfig()
+    for w in (6, 4096):
+        llr, _, _ = noisy_llrs(mm, w, 3.5, seed=6, fixed=False)
+        base = _gpu(mm, llr, cfg, posteriors=False)
+        for scale in (0.25, 4.0):
+            got = _gpu(mm, (llr * np.float32(scale)).astype(np.float32), cfg, posteriors=False)
+            assert np.array_equal(base[0], got[0]) and np.array_equal(base[1], got[1])
 
 
 def test_batch_partition_invariance():
