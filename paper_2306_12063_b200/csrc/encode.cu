@@ -469,18 +469,53 @@ __device__ __forceinline__ BZ<Z> block_of(const uint32_t (&R)[KW]) {   // bits [
   x.w[BZ<Z>::W - 1] &= BZ<Z>::LAST;
   return x;
 }
-template <class S, int Z, int KW, int T, int J>
-__device__ __forceinline__ void accz(BZ<Z>& s, const BZ<Z>& uj) {
-  constexpr int e = entry_at<S>(T, J);
-  if constexpr (e >= 0) bz_xor(s, rotlz<Z, S::SHIFT0[e]>(uj));
+// Periodic expansion of a block: PZ.w[k] = bits [32k, 32k + 32) of the
+// infinite string S[i] = x[i mod Z], so a rotation by E is one funnel shift
+// per word (S[E + 32q ..]); bits past Z in the last word are garbage until the
+// accumulated S_i is masked once (Z >= 16: one wrap per word suffices).
+template <int Z>
+struct PZ {
+  static constexpr int W = BZ<Z>::W, NW = (Z - 1 + 32 * W) / 32 + 1;
+  uint32_t w[NW];
+};
+template <int Z, int O>
+__device__ __forceinline__ uint32_t word_at(const BZ<Z>& x) {   // S[O .. O + 32), 0 <= O < Z
+  static_assert(Z >= 16, "one wrap per word");
+  constexpr int W = BZ<Z>::W, a = O / 32, r = O % 32;
+  auto get = [&](int i) { return i < W ? x.w[i] : 0u; };
+  const uint32_t head = r == 0 ? get(a) : __funnelshift_l(get(a + 1), get(a), r);
+  if constexpr (O + 32 <= Z) return head;
+  else return head | (x.w[0] >> (Z - O));
 }
-template <class S, int Z, int KW, int J, int... Ts>
-__device__ __forceinline__ void colz(BZ<Z> (&s)[S::MB], const BZ<Z>& uj, std::integer_sequence<int, Ts...>) {
-  (accz<S, Z, KW, Ts, J>(s[Ts], uj), ...);
+template <int Z, int... Ks>
+__device__ __forceinline__ PZ<Z> periodic(const BZ<Z>& x, std::integer_sequence<int, Ks...>) {
+  return PZ<Z>{{word_at<Z, (32 * Ks) % Z>(x)...}};
+}
+template <int Z, int E>
+__device__ __forceinline__ void xor_rot(BZ<Z>& s, const PZ<Z>& p) {   // s ^= rotl(x, E), unmasked
+#pragma unroll
+  for (int q = 0; q < BZ<Z>::W; ++q) {
+    constexpr int r = E % 32;
+    const int a = (E + 32 * q) / 32;
+    s.w[q] ^= r == 0 ? p.w[a] : __funnelshift_l(p.w[a + 1], p.w[a], r);
+  }
+}
+template <class S, int Z, int T, int J>
+__device__ __forceinline__ void accz(BZ<Z>& s, const PZ<Z>& pj) {
+  constexpr int e = entry_at<S>(T, J);
+  if constexpr (e >= 0) xor_rot<Z, S::SHIFT0[e]>(s, pj);
+}
+template <class S, int Z, int J, int... Ts>
+__device__ __forceinline__ void colz(BZ<Z> (&s)[S::MB], const PZ<Z>& pj, std::integer_sequence<int, Ts...>) {
+  (accz<S, Z, Ts, J>(s[Ts], pj), ...);
 }
 template <class S, int Z, int KW, int... Js>
 __device__ __forceinline__ void colsz(BZ<Z> (&s)[S::MB], const uint32_t (&R)[KW], std::integer_sequence<int, Js...>) {
-  (colz<S, Z, KW, Js>(s, block_of<S, Z, KW, Js * Z>(R), std::make_integer_sequence<int, S::MB>{}), ...);
+  (colz<S, Z, Js>(s, periodic<Z>(block_of<S, Z, KW, Js * Z>(R), std::make_integer_sequence<int, PZ<Z>::NW>{}),
+                  std::make_integer_sequence<int, S::MB>{}),
+   ...);
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i) s[i].w[BZ<Z>::W - 1] &= BZ<Z>::LAST;
 }
 template <class S, int Z, int T>
 __device__ __forceinline__ void hbz(BZ<Z>& v, const BZ<Z>& v0) {
@@ -507,10 +542,54 @@ __device__ __forceinline__ void chainz(BZ<Z>& v, const BZ<Z>& v0, const BZ<Z> (&
   }
 }
 
+// One codeword: thread `c` of the tile reads its info row from the linear
+// input tile `lin` and streams the codeword row into the zeroed linear output
+// tile `lout` (interior words stored, the two shared words ORed in).
+template <class S>
+__device__ __forceinline__ void zbits_row(const uint32_t* lin, uint32_t* lout, int c) {
+  using T = ZBitsTile<S>;
+  constexpr int Z = T::Z;
+  const uint32_t b0 = (uint32_t)c * T::KBYTES, a0 = b0 >> 2, sh_in = 8 * (b0 & 3);
+  uint32_t R[T::KW];                                       // the info row as big-endian words
+#pragma unroll
+  for (int m = 0; m < T::KW; ++m) R[m] = __funnelshift_l(bswap32(lin[a0 + m + 1]), bswap32(lin[a0 + m]), sh_in);
+  if constexpr (T::K % 32 != 0) R[T::KW - 1] &= ~0u << (32 - T::K % 32);
+  BZ<Z> s[S::MB];
+#pragma unroll
+  for (int i = 0; i < S::MB; ++i)
+#pragma unroll
+    for (int q = 0; q < BZ<Z>::W; ++q) s[i].w[q] = 0;
+  colsz<S, Z, T::KW>(s, R, std::make_integer_sequence<int, S::KB>{});
+  BZ<Z> ssum = s[0];
+#pragma unroll
+  for (int i = 1; i < S::MB; ++i) bz_xor(ssum, s[i]);
+  uint32_t O[T::NW];
+#pragma unroll
+  for (int m = 0; m < T::NW; ++m) O[m] = m < T::KW ? R[m] : 0u;   // systematic bits
+  const BZ<Z> v0 = rotlz<Z, (Z - hb_y_shift<S>()) % Z>(ssum);
+  put_z<Z, T::K>(O, v0);
+  BZ<Z> v = s[0];
+  hbz<S, Z, 0>(v, v0);
+  put_z<Z, T::K + Z>(O, v);
+  chainz<S, Z, 1>(v, v0, s, O);
+  const uint32_t ob = (uint32_t)c * T::NBYTES, w0 = ob >> 2, sh = 8 * (ob & 3);
+#pragma unroll
+  for (int t = 0; t <= T::NW; ++t) {                       // words t = 0 .. NW touched when sh != 0
+    const uint32_t hi = t > 0 ? O[t - 1] : 0u, lo = t < T::NW ? O[t] : 0u;
+    const uint32_t y = bswap32(__funnelshift_r(lo, hi, sh));
+    const bool edge = t == 0 || t >= (int)((sh + 8 * T::NBYTES) >> 5);   // may hold a neighbour's bytes
+    if (edge) {
+      if (y) atomicOr(lout + w0 + t, y);
+    } else {
+      lout[w0 + t] = y;
+    }
+  }
+}
+
+// staged kernel: any alignment, ragged last tile
 template <class S>
 __global__ void __launch_bounds__(kEncThreads) encode_zbits_kernel(const __grid_constant__ EncodeArgs a) {
   using T = ZBitsTile<S>;
-  constexpr int Z = T::Z;
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* lin = reinterpret_cast<uint32_t*>(sm);                  // the tile's info rows, contiguous
   uint32_t* lout = reinterpret_cast<uint32_t*>(sm + T::IN_ALLOC);   // the tile's codeword rows, contiguous
@@ -530,47 +609,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_zbits_kernel(const __grid_
     }
     for (int i = tid; i < T::OUT_ALLOC / 16; i += kEncThreads) reinterpret_cast<uint4*>(lout)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    if (tid < ncw) {
-      // the info row as big-endian words
-      const uint32_t b0 = (uint32_t)tid * T::KBYTES, a0 = b0 >> 2, sh_in = 8 * (b0 & 3);
-      uint32_t R[T::KW];
-#pragma unroll
-      for (int m = 0; m < T::KW; ++m) R[m] = __funnelshift_l(bswap32(lin[a0 + m + 1]), bswap32(lin[a0 + m]), sh_in);
-      if constexpr (T::K % 32 != 0) R[T::KW - 1] &= ~0u << (32 - T::K % 32);
-      BZ<Z> s[S::MB];
-#pragma unroll
-      for (int i = 0; i < S::MB; ++i)
-#pragma unroll
-        for (int q = 0; q < BZ<Z>::W; ++q) s[i].w[q] = 0;
-      colsz<S, Z, T::KW>(s, R, std::make_integer_sequence<int, S::KB>{});
-      BZ<Z> ssum = s[0];
-#pragma unroll
-      for (int i = 1; i < S::MB; ++i) bz_xor(ssum, s[i]);
-      uint32_t O[T::NW];
-#pragma unroll
-      for (int m = 0; m < T::NW; ++m) O[m] = m < T::KW ? R[m] : 0u;   // systematic bits
-      const BZ<Z> v0 = rotlz<Z, (Z - hb_y_shift<S>()) % Z>(ssum);
-      put_z<Z, T::K>(O, v0);
-      BZ<Z> v = s[0];
-      hbz<S, Z, 0>(v, v0);
-      put_z<Z, T::K + Z>(O, v);
-      chainz<S, Z, 1>(v, v0, s, O);
-      // stream the row into the linear tile at bit offset 8 c NBYTES
-      const uint32_t ob = (uint32_t)tid * T::NBYTES, w0 = ob >> 2, sh = 8 * (ob & 3);
-      constexpr int LAST_T = T::NW;                          // words t = 0 .. NW touched when sh != 0
-#pragma unroll
-      for (int t = 0; t <= LAST_T; ++t) {
-        const uint32_t hi = t > 0 ? O[t - 1] : 0u, lo = t < T::NW ? O[t] : 0u;
-        const uint32_t y = bswap32(__funnelshift_r(lo, hi, sh));
-        // first / last words may hold a neighbour's bytes: OR them in
-        const bool edge = t == 0 || t >= (int)((sh + 8 * T::NBYTES) >> 5);
-        if (edge) {
-          if (y) atomicOr(lout + w0 + t, y);
-        } else {
-          lout[w0 + t] = y;
-        }
-      }
-    }
+    if (tid < ncw) zbits_row<S>(lin, lout, tid);
     __syncthreads();
     uint8_t* gout = a.cw + cw0 * T::NBYTES;
     if (out_al && full) {
@@ -582,6 +621,57 @@ __global__ void __launch_bounds__(kEncThreads) encode_zbits_kernel(const __grid_
     }
     __syncthreads();
   }
+}
+
+// Bulk-copy pipeline (whole 16-byte-aligned tiles): info tiles arrive by
+// cp.async.bulk into a double buffer completing on mbarriers, codeword tiles
+// leave by one bulk store each, so tile i+1's load and tile i-1's store
+// overlap tile i's encoding (as encode_z96_kernel).
+template <class S>
+struct ZBitsPipe {
+  using T = ZBitsTile<S>;
+  static constexpr int IN_ALLOC = T::IN_ALLOC, OUT_ALLOC = T::OUT_ALLOC;
+  static constexpr size_t SMEM = 2 * (size_t)IN_ALLOC + OUT_ALLOC + 16;
+};
+template <class S>
+__global__ void __launch_bounds__(kEncThreads) encode_zbits_tma_kernel(const __grid_constant__ EncodeArgs a) {
+  using T = ZBitsTile<S>;
+  using PP = ZBitsPipe<S>;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint8_t* inbuf = sm;                                     // 2 x IN_ALLOC
+  uint32_t* lout = reinterpret_cast<uint32_t*>(sm + 2 * PP::IN_ALLOC);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * PP::IN_ALLOC + PP::OUT_ALLOC);
+  const int64_t tiles = a.w / kEncThreads;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int b = 0; b < 2; ++b) {
+      const int64_t tl = blockIdx.x + (int64_t)b * gridDim.x;
+      if (tl < tiles) bulk_load(inbuf + b * PP::IN_ALLOC, a.info + tl * T::IN_BYTES, T::IN_BYTES, &bar[b]);
+    }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (tid == 0) bulk_wait_read();                        // the previous store has left lout
+    __syncthreads();
+    for (int i = tid; i < PP::OUT_ALLOC / 16; i += kEncThreads) reinterpret_cast<uint4*>(lout)[i] = make_uint4(0, 0, 0, 0);
+    mbar_wait(&bar[b], (uint32_t)((it >> 1) & 1));
+    __syncthreads();
+    zbits_row<S>(reinterpret_cast<const uint32_t*>(inbuf + b * PP::IN_ALLOC), lout, tid);
+    fence_async_smem();                                    // generic-proxy writes -> bulk store
+    __syncthreads();                                       // lout complete, inbuf[b] consumed
+    if (tid == 0) {
+      bulk_store(a.cw + tile * T::OUT_BYTES, lout, T::OUT_BYTES);
+      const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
+      if (nxt < tiles) bulk_load(inbuf + b * PP::IN_ALLOC, a.info + nxt * T::IN_BYTES, T::IN_BYTES, &bar[b]);
+    }
+  }
+  if (tid == 0) bulk_wait_all();
 }
 
 static int64_t enc_grid(const void* kern, size_t smem, int64_t tiles, cudaError_t* err) {
@@ -632,9 +722,25 @@ template <class S>
 static cudaError_t launch_zbits(const EncodeArgs& a, cudaStream_t s) {
   using T = ZBitsTile<S>;
   cudaError_t e = cudaSuccess;
-  const int64_t grid = enc_grid((const void*)encode_zbits_kernel<S>, T::SMEM, (a.w + kEncThreads - 1) / kEncThreads, &e);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.info) | reinterpret_cast<uintptr_t>(a.cw)) & 15) == 0;
+  const int64_t full = aligned ? a.w / kEncThreads * kEncThreads : 0;
+  if (full > 0) {
+    const size_t smem = ZBitsPipe<S>::SMEM;
+    const int64_t grid = enc_grid((const void*)encode_zbits_tma_kernel<S>, smem, full / kEncThreads, &e);
+    if (e != cudaSuccess) return e;
+    EncodeArgs b = a;
+    b.w = full;
+    encode_zbits_tma_kernel<S><<<(unsigned)grid, kEncThreads, smem, s>>>(b);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (full == a.w) return cudaSuccess;
+  EncodeArgs r = a;
+  r.info = a.info + full * T::KBYTES;
+  r.cw = a.cw + full * T::NBYTES;
+  r.w = a.w - full;
+  const int64_t grid = enc_grid((const void*)encode_zbits_kernel<S>, T::SMEM, (r.w + kEncThreads - 1) / kEncThreads, &e);
   if (e != cudaSuccess) return e;
-  encode_zbits_kernel<S><<<(unsigned)grid, kEncThreads, T::SMEM, s>>>(a);
+  encode_zbits_kernel<S><<<(unsigned)grid, kEncThreads, T::SMEM, s>>>(r);
   return cudaGetLastError();
 }
 

@@ -428,3 +428,16 @@ def test_bit_granular_encoder_codewords_satisfy_h():
         syn = np.zeros((cw.shape[0], h.m), np.uint8)
         np.bitwise_xor.at(syn.T, rows, cw[:, h.row_cols].T)
         assert not syn.any(), (mm.n, mm.z)
+
+
+@pytest.mark.parametrize("n,rate", [(648, "1/2"), (1296, "2/3"), (1944, "5/6")])
+def test_bit_granular_encoder_pipeline_many_tiles(n, rate):
+    """Native Wi-Fi codes stream whole 128-codeword tiles through the bulk-copy
+    pipeline (several tiles per CTA: both buffer parities) and the ragged tail
+    through the staged kernel."""
+    mm = P.get_model_matrix("wifi", n, rate)
+    rng = np.random.default_rng(n)
+    bits = rng.integers(0, 2, size=(128 * 1200 + 77, mm.k), dtype=np.uint8)
+    want = P.pack_bits(P.encode_array(P.make_plan(mm), bits))
+    got = P.encode_bits(mm, torch.from_numpy(P.pack_bits(bits)).cuda()).cpu().numpy()
+    assert np.array_equal(got, want)
