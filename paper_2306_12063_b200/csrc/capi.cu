@@ -51,6 +51,7 @@ struct qc_code_s {
   int32_t mb = 0, nb = 0, kb = 0, z = 0, n = 0, ne = 0, max_deg = 0;
   int32_t structure = -1;            // index into kStructureMasks, -1 = generic only
   bool native = false;               // structure's own Z0 and SHIFT0 (compile-time shift kernels)
+  bool scaled = false;               // WiMAX structure with the standard scaled shifts at z
   std::vector<int32_t> shifts;       // mb x nb
   std::vector<int32_t> tier_start, ent_j, ent_e;
   int32_t enc_y = -1, enc_hb = -1;   // encoder plan (find_y, encoder.py:39-46), -1 if malformed
@@ -111,6 +112,7 @@ int build_code(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code
     if (same && z * 1 <= 384) { c->structure = s; break; }
   }
   if (c->structure >= 0) c->native = spec_is_native(c->structure, z, c->ent_e.data(), c->ne);
+  if (c->structure >= 0) c->scaled = spec_is_scaled(c->structure, z, c->ent_e.data(), c->ne);
   // encoder plan: the single interior non-negative entry of the h_b column
   if (mb >= 3) {
     int y = -1, cnt = 0;
@@ -414,6 +416,7 @@ int qc_encode_packed(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw, v
   memset(&a, 0, sizeof a);
   a.info = info; a.cw = cw; a.w = w; a.mb = c->mb; a.nb = c->nb; a.z = c->z; a.hb_shift = c->enc_hb;
   a.native = c->native ? 1 : 0;
+  a.scaled = c->scaled ? 1 : 0;
   for (int i = 0; i < c->mb * c->nb; ++i) a.shifts[i] = c->shifts[i];
   cudaError_t e = launch_encode_packed(a, c->structure, as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "encode_packed");
@@ -434,6 +437,7 @@ int qc_encode_bits(qc_code_t c, const uint8_t* info, int64_t w, uint8_t* cw, voi
   a.info = info; a.cw = cw; a.w = w; a.mb = c->mb; a.nb = c->nb; a.z = c->z; a.hb_shift = c->enc_hb;
   for (int i = 0; i < c->mb * c->nb; ++i) a.shifts[i] = c->shifts[i];
   a.native = c->native ? 1 : 0;
+  a.scaled = c->scaled ? 1 : 0;
   cudaError_t e = launch_encode_packed(a, c->structure, as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "encode_bits");
   return QC_OK;

@@ -45,6 +45,23 @@ bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne) {
   return native;
 }
 
+bool spec_is_scaled(int structure_id, int z, const int32_t* ent_e, int ne) {
+  bool scaled = false;
+#define QCB_SCL(STRUCT)                                                                 \
+  if (structure_id == STRUCT::ID && STRUCT::Z0 == 96 && z >= 24 && z <= 96 && z % 4 == 0 && \
+      ne == STRUCT::NE) {                                                                \
+    scaled = true;                                                                       \
+    for (int i = 0; i < ne; ++i) {                                                       \
+      const int p = STRUCT::SHIFT0[i];                                                   \
+      const int want = p <= 0 ? p : (STRUCT::ID == S_wimax_r23a::ID ? p % z : p * z / 96); \
+      scaled = scaled && ent_e[i] == want;                                               \
+    }                                                                                    \
+  }
+  QCB_FOR_EACH_STRUCTURE(QCB_SCL)
+#undef QCB_SCL
+  return scaled;
+}
+
 void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
                int32_t* pair16) {
   int ne = 0, maxdeg = 0;

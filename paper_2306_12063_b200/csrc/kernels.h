@@ -52,6 +52,8 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
                int32_t* pair16);
 // true when (z, tier-major shifts) equal the structure's native Z0 / SHIFT0 tables
 bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne);
+// a WiMAX structure whose shifts are the standard scaling of its Z0 = 96 table to z
+bool spec_is_scaled(int structure_id, int z, const int32_t* ent_e, int ne);
 
 // Packed direct encoder (encoder.py:166-199), byte-aligned Z.
 struct EncodeArgs {
@@ -60,6 +62,7 @@ struct EncodeArgs {
   int64_t w;
   int32_t mb, nb, z, hb_shift;
   int32_t native;           // 1: shifts are the structure's native SHIFT0 at Z0
+  int32_t scaled;           // 1: WiMAX structure, shifts = the 802.16e scaling of SHIFT0 to z
   int32_t shifts[12 * 24];  // mb x nb, -1 = zero block
 };
 // structure_id: index into kStructureMasks, -1 = generic

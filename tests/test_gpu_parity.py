@@ -430,12 +430,14 @@ def test_bit_granular_encoder_codewords_satisfy_h():
         assert not syn.any(), (mm.n, mm.z)
 
 
-@pytest.mark.parametrize("n,rate", [(648, "1/2"), (1296, "2/3"), (1944, "5/6")])
-def test_bit_granular_encoder_pipeline_many_tiles(n, rate):
-    """Native Wi-Fi codes stream whole 128-codeword tiles through the bulk-copy
-    pipeline (several tiles per CTA: both buffer parities) and the ragged tail
-    through the staged kernel."""
-    mm = P.get_model_matrix("wifi", n, rate)
+@pytest.mark.parametrize("std,n,rate", [("wifi", 648, "1/2"), ("wifi", 1296, "2/3"), ("wifi", 1944, "5/6"),
+                                        ("wimax", 576, "2/3A"), ("wimax", 1344, "3/4B"), ("wimax", 2208, "5/6")])
+def test_bit_granular_encoder_pipeline_many_tiles(std, n, rate):
+    """Native Wi-Fi codes and scaled WiMAX codes (compile-time scaled shifts)
+    stream whole 128-codeword tiles through the bulk-copy pipeline (several
+    tiles per CTA: both buffer parities), the ragged tail through the staged
+    kernel."""
+    mm = P.get_model_matrix(std, n, rate)
     rng = np.random.default_rng(n)
     bits = rng.integers(0, 2, size=(128 * 1200 + 77, mm.k), dtype=np.uint8)
     want = P.pack_bits(P.encode_array(P.make_plan(mm), bits))
