@@ -403,6 +403,8 @@ def run_ours(args, wl):
                          "hbm": {"achieved": round(hbm_ach, 1), "peak": peaks.get("hbm_gbs"),
                                  "unit": "GB/s", "frac": round(hbm_ach / peaks.get("hbm_gbs", 6650.0), 4)}},
             "gpu_launches": args.steps * len(codes),
+            # information-bit rate (coded x K/N), the unit the paper quotes its throughput in
+            "info_gbit_s": round(value * sum(m.k for m in mms) / sum(m.n for m in mms), 4),
             "clocks": clocks.summary(),
             "counters": {"bit_errors": cnt[0], "frame_errors": cnt[1], "iter_sum": cnt[2],
                          "converged": cnt[3], "frames": cnt[4],
