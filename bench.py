@@ -290,6 +290,9 @@ def run_ours(args, wl):
     stream = torch.cuda.Stream(dev)
 
     def step():
+        if len(codes) > 1:                     # C4: one grouped call, the codes decode concurrently
+            P.decode_grouped(list(zip(codes, llrs)), cfg, out=outs, stream=stream)
+            return
         for c, t, o in zip(codes, llrs, outs):
             P.decode_batch(c, t, cfg, out=o, stream=stream)
 

@@ -78,7 +78,10 @@ int qc_decode_i16(qc_code_t code, const int16_t* llr, int64_t w, int32_t max_ite
                   int32_t early_term, uint8_t* hard, int32_t hard_packed, int32_t* iters,
                   uint8_t* conv, int16_t* post_out, void* cuda_stream);
 
-/* ---- mixed-code batch: one job per code, all on one stream --------------- */
+/* ---- mixed-code batch: one job per code.  Every job is validated first; the
+ * jobs then fork from cuda_stream onto side streams and join back (stream
+ * ordered, graph-capturable), so the codes decode concurrently.  Set
+ * QCB_GROUPED_SERIAL=1 to queue them one after another on cuda_stream. */
 typedef struct {
   qc_code_t code;
   const void* llr;   /* device, w x n float32 or int16 (per call) */

@@ -363,29 +363,108 @@ int qc_decode_i16(qc_code_t code, const int16_t* llr, int64_t w, int32_t max_ite
                                 post_out, as_stream(stream));
 }
 
-static int grouped(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
-                   int32_t hard_packed, void* stream, bool f32) {
-  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(QC_EINVAL, "bad job list");
-  for (int i = 0; i < n_jobs; ++i) {
-    const qc_decode_job_t& j = jobs[i];
-    const int rc = f32 ? decode_device<float>(j.code, (const float*)j.llr, j.w, max_iters, early_term, j.hard,
-                                              hard_packed, j.iters, j.conv, (float*)j.post_out, as_stream(stream))
-                       : decode_device<int16_t>(j.code, (const int16_t*)j.llr, j.w, max_iters, early_term,
-                                                j.hard, hard_packed, j.iters, j.conv, (int16_t*)j.post_out,
-                                                as_stream(stream));
-    if (rc) return rc;
+}  // extern "C"
+
+namespace {
+
+// Per-device side streams for the grouped launch (created once, never freed).
+constexpr int kGroupStreams = 8;
+cudaStream_t* group_streams(int device, cudaError_t* err) {
+  static std::mutex m;
+  static std::map<int, std::vector<cudaStream_t>> all;
+  std::lock_guard<std::mutex> lk(m);
+  auto& v = all[device];
+  if (v.empty()) {
+    for (int i = 0; i < kGroupStreams; ++i) {
+      cudaStream_t s = nullptr;
+      *err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (*err != cudaSuccess) return nullptr;
+      v.push_back(s);
+    }
   }
+  *err = cudaSuccess;
+  return v.data();
+}
+
+template <typename T>
+int validate_job(const qc_decode_job_t& j, int32_t max_iters) {
+  if (!j.code) return fail(QC_EINVAL, "code is NULL");
+  if (j.w < 0 || max_iters < 0) return fail(QC_EINVAL, "w=%lld max_iters=%d", (long long)j.w, max_iters);
+  if (j.w > 0 && (!j.llr || !j.hard || !j.iters || !j.conv)) return fail(QC_EINVAL, "NULL buffer");
   return QC_OK;
 }
 
+// Mixed-code batch.  Every job is validated before any work is queued; the
+// jobs then fork from the caller's stream onto per-device side streams
+// (event record / wait, so the call stays stream-ordered and can be captured
+// into a CUDA graph) and join back, so the codes' kernels run concurrently:
+// the tail wave of one code's grid overlaps the next code's CTAs.
+template <typename T>
+int grouped(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
+            int32_t hard_packed, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(QC_EINVAL, "bad job list");
+  for (int i = 0; i < n_jobs; ++i) {
+    const int rc = validate_job<T>(jobs[i], max_iters);
+    if (rc) return rc;
+  }
+  auto run = [&](const qc_decode_job_t& j, cudaStream_t s) {
+    return decode_device<T>(j.code, (const T*)j.llr, j.w, max_iters, early_term, j.hard, hard_packed, j.iters,
+                            j.conv, (T*)j.post_out, s);
+  };
+  const cudaStream_t origin = as_stream(stream);
+  if (n_jobs <= 1 || std::getenv("QCB_GROUPED_SERIAL")) {
+    for (int i = 0; i < n_jobs; ++i) {
+      const int rc = run(jobs[i], origin);
+      if (rc) return rc;
+    }
+    return QC_OK;
+  }
+  int device = 0;
+  cudaError_t e = cudaGetDevice(&device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  cudaStream_t* side = group_streams(device, &e);
+  if (!side) return cuda_fail(e, "side streams");
+  const int ns = std::min<int>(n_jobs, kGroupStreams);
+  cudaEvent_t ev[kGroupStreams + 1];
+  int made = 0, rc = QC_OK;
+  for (; made < ns + 1; ++made) {
+    e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaEventCreate"); break; }
+  }
+  if (!rc) {
+    e = cudaEventRecord(ev[ns], origin);
+    for (int k = 0; k < ns && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(side[k], ev[ns], 0);
+    if (e != cudaSuccess) rc = cuda_fail(e, "fork");
+  }
+  // largest jobs first, round-robin over the side streams
+  std::vector<int> order(n_jobs);
+  for (int i = 0; i < n_jobs; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return jobs[a].w * (int64_t)jobs[a].code->ne * jobs[a].code->z > jobs[b].w * (int64_t)jobs[b].code->ne * jobs[b].code->z;
+  });
+  for (int q = 0; q < n_jobs && !rc; ++q) rc = run(jobs[order[q]], side[q % ns]);
+  // join (also after a failure, so no side stream is left ahead of the caller)
+  for (int k = 0; k < ns && made == ns + 1; ++k) {
+    e = cudaEventRecord(ev[k], side[k]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(origin, ev[k], 0);
+    if (e != cudaSuccess && !rc) rc = cuda_fail(e, "join");
+  }
+  for (int k = 0; k < made; ++k) cudaEventDestroy(ev[k]);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
 int qc_decode_grouped_f32(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
                           int32_t hard_packed, void* stream) {
-  return grouped(jobs, n_jobs, max_iters, early_term, hard_packed, stream, true);
+  return grouped<float>(jobs, n_jobs, max_iters, early_term, hard_packed, stream);
 }
 
 int qc_decode_grouped_i16(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t max_iters, int32_t early_term,
                           int32_t hard_packed, void* stream) {
-  return grouped(jobs, n_jobs, max_iters, early_term, hard_packed, stream, false);
+  return grouped<int16_t>(jobs, n_jobs, max_iters, early_term, hard_packed, stream);
 }
 
 int qc_decode_batch_f32_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,

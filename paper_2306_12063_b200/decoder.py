@@ -260,6 +260,29 @@ def code_handle(code) -> _lib.Code:
     return c
 
 
+def _check_llrs(t, c, cfg):
+    import torch
+    if t.dim() != 2 or t.shape[1] != c.n:
+        raise SizeMismatch(f"llrs must be (W, {c.n}), got {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise ValueError("torch input must be a CUDA tensor")
+    want = torch.float32 if cfg.arithmetic is Arithmetic.Float32 else torch.int16
+    if t.dtype != want:
+        raise ArithmeticMismatch(f"llr dtype {t.dtype} != {want} for {cfg.arithmetic.value}")
+
+
+def _check_out(hard, iters, conv, w, n, hard_packed, device):
+    """Caller-provided outputs must have exactly the shapes, dtypes and device
+    the kernels write (they are raw pointers on the C side)."""
+    import torch
+    want = ((hard, (w, (n + 7) // 8 if hard_packed else n), torch.uint8, "hard"),
+            (iters, (w,), torch.int32, "iters"), (conv, (w,), torch.uint8, "conv"))
+    for t, shape, dtype, name in want:
+        if tuple(t.shape) != shape or t.dtype != dtype or t.device != device or not t.is_contiguous():
+            raise SizeMismatch(f"out {name}: need contiguous {dtype} {shape} on {device}, "
+                               f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+
+
 def decode_batch(code, llrs, cfg: DecoderConfig | None = None, *, hard_packed: bool = False,
                  posteriors: bool = False, out=None, stream=None):
     """Decode a (W, N) batch; returns (hard, iters, conv[, post]).
@@ -284,13 +307,7 @@ def decode_batch(code, llrs, cfg: DecoderConfig | None = None, *, hard_packed: b
         return tuple(t.cpu().numpy() for t in res)
     import torch
     t = llrs
-    if t.dim() != 2 or t.shape[1] != c.n:
-        raise SizeMismatch(f"llrs must be (W, {c.n}), got {tuple(t.shape)}")
-    if not t.is_cuda:
-        raise ValueError("torch input must be a CUDA tensor")
-    want = torch.float32 if cfg.arithmetic is Arithmetic.Float32 else torch.int16
-    if t.dtype != want:
-        raise ArithmeticMismatch(f"llr dtype {t.dtype} != {want} for {cfg.arithmetic.value}")
+    _check_llrs(t, c, cfg)
     t = t.contiguous()
     w = t.shape[0]
     dev = t.device
@@ -301,7 +318,11 @@ def decode_batch(code, llrs, cfg: DecoderConfig | None = None, *, hard_packed: b
         post = torch.empty_like(t) if posteriors else None
     else:
         hard, iters, conv = out[:3]
+        _check_out(hard, iters, conv, w, c.n, hard_packed, dev)
         post = out[3] if posteriors else None
+        if post is not None and (post.shape != t.shape or post.dtype != t.dtype or post.device != dev
+                                 or not post.is_contiguous()):
+            raise SizeMismatch(f"out post: need contiguous {t.dtype} {tuple(t.shape)} on {dev}")
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = _lib.lib().qc_decode_f32 if cfg.arithmetic is Arithmetic.Float32 else _lib.lib().qc_decode_i16
     _lib.check(fn(c.handle, _lib.ptr(t), w, cfg.max_iterations, 1 if cfg.early_termination else 0,
@@ -310,20 +331,30 @@ def decode_batch(code, llrs, cfg: DecoderConfig | None = None, *, hard_packed: b
     return (hard, iters, conv, post) if posteriors else (hard, iters, conv)
 
 
-def decode_grouped(jobs, cfg: DecoderConfig | None = None, *, hard_packed: bool = False, stream=None):
+def decode_grouped(jobs, cfg: DecoderConfig | None = None, *, hard_packed: bool = False, stream=None,
+                   out=None):
     """Mixed-code batch (BASELINE config 4): `jobs` is a list of (code, llr_tensor)
-    pairs on one CUDA device; returns a list of (hard, iters, conv) per job."""
+    pairs on one CUDA device; returns a list of (hard, iters, conv) per job
+    (`out`: optional preallocated list of such triples).  One call: the codes
+    decode concurrently on side streams forked from `stream` and joined back."""
     import torch
     cfg = cfg or DecoderConfig()
+    if out is not None and len(out) != len(jobs):
+        raise ValueError("out must hold one (hard, iters, conv) triple per job")
     outs, arr = [], (_lib.DecodeJob * len(jobs))()
     keep = []
     for i, (code, t) in enumerate(jobs):
         c = code_handle(code)
+        _check_llrs(t, c, cfg)
         t = t.contiguous()
         w = t.shape[0]
-        hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=t.device)
-        iters = torch.empty(w, dtype=torch.int32, device=t.device)
-        conv = torch.empty(w, dtype=torch.uint8, device=t.device)
+        if out is not None:
+            hard, iters, conv = out[i]
+            _check_out(hard, iters, conv, w, c.n, hard_packed, t.device)
+        else:
+            hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=t.device)
+            iters = torch.empty(w, dtype=torch.int32, device=t.device)
+            conv = torch.empty(w, dtype=torch.uint8, device=t.device)
         arr[i] = _lib.DecodeJob(c.handle.value, t.data_ptr(), w, hard.data_ptr(), iters.data_ptr(),
                                 conv.data_ptr(), None)
         outs.append((hard, iters, conv))

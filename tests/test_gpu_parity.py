@@ -119,6 +119,79 @@ def test_all_126_codes_match_oracle(fixed, early):
         assert _post_equal(post, op), (std, n, rate)
 
 
+C4_CODES = [("wifi", n, r) for n in (648, 1296, 1944) for r in ("1/2", "2/3", "3/4", "5/6")] + \
+    [("wimax", 2304, r) for r in ("1/2", "2/3A", "2/3B", "3/4A", "3/4B", "5/6")]
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+@pytest.mark.parametrize("early", [False, True])
+def test_grouped_mixed_code_batch_matches_oracle(fixed, early):
+    """BASELINE config 4's shape: all 18 codes (plus an empty job and a
+    generic-kernel code) in ONE decode_grouped call, the jobs running
+    concurrently on side streams; every job bit-identical to the oracle and
+    to the serial per-code path."""
+    rng = np.random.default_rng(41 + 2 * fixed + early)
+    arith = P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32
+    cfg = P.DecoderConfig(max_iterations=5, arithmetic=arith, early_termination=early)
+    mms = [P.get_model_matrix(*c) for c in C4_CODES]
+    ent = rng.integers(-1, 17, size=(4, 10))
+    ent[:, 0] = rng.integers(0, 17, size=4)
+    mms.append(P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 17, 10, 6, ent))      # generic kernel
+    jobs, llrs = [], []
+    for i, mm in enumerate(mms):
+        w = 0 if i == 3 else 23 + 3 * i                                         # job 3 is empty
+        if i < len(C4_CODES):
+            llr, _, _ = noisy_llrs(mm, max(w, 1), 1.5 + 2.0 * mm.rate.fraction, seed=900 + i, fixed=fixed)
+            llr = llr[:w]
+        elif fixed:
+            llr = rng.integers(-600, 600, size=(w, mm.n)).astype(np.int16)
+        else:
+            llr = (rng.standard_normal((w, mm.n)) * 2).astype(np.float32)
+        llrs.append(llr)
+        jobs.append((mm, torch.from_numpy(np.ascontiguousarray(llr)).cuda()))
+    outs = P.decode_grouped(jobs, cfg)
+    torch.cuda.synchronize()
+    for (mm, t), llr, (hard, it, conv) in zip(jobs, llrs, outs):
+        assert hard.shape == (llr.shape[0], mm.n)
+        if llr.shape[0] == 0:
+            continue
+        oh, oi, oc = O.decode_batch(P.expand(mm), llr, 5, early, workers=4)
+        assert np.array_equal(hard.cpu().numpy(), oh), mm
+        assert np.array_equal(it.cpu().numpy(), oi) and np.array_equal(conv.cpu().numpy(), oc), mm
+        serial = P.decode_batch(mm, t, cfg)
+        for a, b in zip(serial, (hard, it, conv)):
+            assert torch.equal(a, b)
+
+
+def test_grouped_batch_graph_capture_and_preallocated_outputs():
+    """The grouped call is stream-ordered: captured into a CUDA graph (fork /
+    join of the side streams inside the capture) it replays to the same
+    outputs; packed hard decisions equal np.packbits of the unpacked ones."""
+    cfg = P.DecoderConfig(max_iterations=4, early_termination=False)
+    mms = [P.get_model_matrix(*c) for c in C4_CODES[::3]]
+    jobs = []
+    for i, mm in enumerate(mms):
+        llr, _, _ = noisy_llrs(mm, 40 + i, 2.5, seed=70 + i)
+        jobs.append((mm, torch.from_numpy(llr).cuda()))
+    ref = P.decode_grouped(jobs, cfg)
+    packed = P.decode_grouped(jobs, cfg, hard_packed=True)
+    torch.cuda.synchronize()
+    outs = [tuple(torch.zeros_like(x) for x in o) for o in ref]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        P.decode_grouped(jobs, cfg, out=outs, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    for (mm, _), a, b, pk in zip(jobs, ref, outs, packed):
+        for x, y in zip(a, b):
+            assert torch.equal(x, y)
+        assert np.array_equal(pk[0].cpu().numpy(), np.packbits(a[0].cpu().numpy(), axis=1))
+    with pytest.raises(P.SizeMismatch):
+        P.decode_grouped(jobs, cfg, out=[(o[0][:, :-1], o[1], o[2]) for o in outs])
+
+
 def test_generic_kernel_on_nonstandard_codes():
     """Codes outside the 18 standard structures take the generic kernel."""
     rng = np.random.default_rng(7)
