@@ -13,7 +13,15 @@ namespace qcb {
 
 constexpr int kMaxDeg = 32;          // sign bitmap width (reference decoder.py:185-186)
 constexpr int kMaxGenericTiers = 256;
-constexpr int kRowStrideUnits = 25;  // padded nb (24 -> 25): odd stride, conflict-free banks
+// Shared-memory posterior layout of the specialised decoders: cell (c, j),
+// i.e. bit n = j Z + c of a codeword, at byte 4 n of the codeword's block --
+// the codeword's own bit order, so the prologue / epilogue are streaming
+// copies.  A tier's Z rows read cells (c = (r + e) mod Z, j): consecutive c,
+// consecutive words, one bank each (the same property the previous [c][j]
+// layout with an odd row stride had).  Every standard structure has nb = 24.
+constexpr int kCellBytes = 4;
+constexpr int kStdNb = 24;
+__host__ __device__ constexpr int cw_block_bytes(int z) { return kStdNb * z * kCellBytes; }   // multiple of 16
 
 // ---- exact float32 helpers -------------------------------------------------
 __device__ __forceinline__ float f_inf() { return __int_as_float(0x7f800000); }

@@ -229,14 +229,12 @@ struct ArithF32 {
 // ---------------------------------------------------------------------------
 // addressing
 // ---------------------------------------------------------------------------
-template <class A>
-constexpr int row_stride_bytes() { return kRowStrideUnits * A::kElem; }
 
 template <class S, class A, int ZS, int E>
 __device__ __forceinline__ uint32_t edge_addr(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
   if constexpr (ZS > 0) {
     constexpr int sh = S::SHIFT0[E];
-    constexpr uint32_t off = (uint32_t)((sh * kRowStrideUnits + S::COL[E]) * A::kElem);
+    constexpr uint32_t off = (uint32_t)((S::COL[E] * ZS + sh) * A::kElem);   // cell (c = r + sh, j)
     if constexpr (sh == 0) return b0 + off;
     else return (r >= ZS - sh ? b1 : b0) + off;
   } else {
@@ -676,7 +674,7 @@ template <class S, class A, int ZS>
 constexpr int reg_cap() {
   const int want = SmemMsg<S>::in_regs() + QCB_REG_SLACK;
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, want, (z * kRowStrideUnits * A::kElem + 15) & ~15, false);
+  return raise_cap(z, want, cw_block_bytes(z), false);
 }
 
 template <class S, class A, int ZS, bool ET>
@@ -684,7 +682,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
     decode_layered_kernel(const __grid_constant__ SpecArgs a) {
   using L = Layered<S, A, ZS>;
   using Val = typename A::Val;
-  constexpr int RS = row_stride_bytes<A>();
+  static_assert(A::kElem == kCellBytes, "4-byte cells");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[kLayMaxCw], s_done[kLayMaxCw], s_iters[kLayMaxCw];
   __shared__ int s_active;
@@ -698,7 +696,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int g = tid / Z, r = tid - g * Z;
   const int64_t cw0 = (int64_t)blockIdx.x * G;
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
-  const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);   // bytes per codeword block
+  const uint32_t cws = (uint32_t)cw_block_bytes(Z);      // bytes per codeword block
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
   // warp: same row, same inputs, same instruction stream, so in lockstep they
@@ -710,9 +708,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int gs = rm.g, rs = rm.r;
   const bool act = gs < ncw;
   // opaque copies keep the row bases in registers (no per-tier rematerialisation)
-  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
+  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * kCellBytes), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
-  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * kCellBytes)));   // c = r + e - Z
   // this thread's address table (after the G posterior blocks)
   const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
   fill_addr_tab<S, A, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
@@ -722,9 +720,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 #pragma unroll
   for (int q = 0; q < SmemMsg<S>::words() / 4; ++q) sts128f(mbase + 16u * q, 0.0f, 0.0f, 0.0f, 0.0f);
 
-  // ---- channel LLRs -> [cw][c][j] --------------------------------------------
+  // ---- channel LLRs -> the codewords' blocks (bit order) ----------------------
   {
-    load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
+    load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -794,7 +792,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   }
   uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
   float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
-  store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
+  store_outputs_cell32<io_cells8<ZS>()>(hard, a.hard_packed, post, ncw, N, sbase,
                        [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
                        [](uint32_t v) { return __uint_as_float(v); });
 }
@@ -807,15 +805,16 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
   }();
   if (env_v >= 1 && env_v <= kLayMaxCw && env_v * z <= kLayMaxThreads) return env_v;
   const int sms = device_sm_count();
-  const int cw_smem = (z * kRowStrideUnits * cell_bytes + 15) & ~15;
+  (void)cell_bytes;
+  const int cw_smem = cw_block_bytes(z);
   return plan_cw_per_cta(z, regs, cw_smem, (double)w / sms);
 }
 
 template <class K>
-inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs, cudaStream_t s, int tab_bytes = 0,
+inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, cudaStream_t s, int tab_bytes = 0,
                                         int msg_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (((size_t)a.pairs * ((z * rs + 15) & ~15) + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
+  const size_t smem = (((size_t)a.pairs * cw_block_bytes(z) + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
                       (size_t)threads * msg_bytes;
   cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
@@ -827,7 +826,6 @@ inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, int rs
 
 template <class S, class A, int ZS, bool ET>
 inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
-  constexpr int RS = row_stride_bytes<A>();
   const int z = ZS > 0 ? ZS : a.z;
   auto kern = decode_layered_kernel<S, A, ZS, ET>;
   // the CTA shape is planned from the register count ptxas actually gave
@@ -839,7 +837,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
-  return launch_layered_fixed(kern, b, z, RS, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
+  return launch_layered_fixed(kern, b, z, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
                               SmemMsg<S>::words() * 4);
 }
 

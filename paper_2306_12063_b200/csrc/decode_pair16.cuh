@@ -250,7 +250,7 @@ struct Layered2 {
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, S::NE + QCB_P16_SLACK, (z * kRowStrideUnits * 4 + 15) & ~15, true);
+  return raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true);
 }
 
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
@@ -258,7 +258,6 @@ template <class S, int ZS, bool ET>
 __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS>()))
     decode_pair16_kernel(const __grid_constant__ SpecArgs a) {
   using L = Layered2<S, ZS>;
-  constexpr int RS = row_stride_bytes<ArithI16x2>();
   constexpr int MAXC = 2 * kLayMaxCw;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
@@ -274,7 +273,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const int64_t cw0 = (int64_t)blockIdx.x * (2 * G);
   const int ncw = (int)(a.w - cw0 < (int64_t)(2 * G) ? a.w - cw0 : (int64_t)(2 * G));
   const int npairs = (ncw + 1) >> 1;
-  const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);
+  const uint32_t cws = (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
   // warp: same row, same inputs, same instruction stream, so in lockstep they
@@ -285,9 +284,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const RowMap rm = map_row(tid, G, Z);
   const int gs = rm.g, rs = rm.r;
   const bool act = gs < npairs;
-  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * RS), b1;
+  uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * kCellBytes), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
-  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * kCellBytes)));
   const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
   // early-termination snapshot block (G == 1), after the address tables
   const uint32_t snap_offset = ((uint32_t)G * cws + blockDim.x * (uint32_t)addr_tab_bytes_per_thread<S, ZS, L::TAB>() +
@@ -296,7 +295,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
-    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
+    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase);
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -401,12 +400,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
   store_outputs_pair16(reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N), a.hard_packed,
-                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, Z, sbase, cws, RS);
+                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, sbase);
 }
 
 template <class S, int ZS, bool ET>
 inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
-  constexpr int RS = row_stride_bytes<ArithI16x2>();
   const int z = ZS > 0 ? ZS : a.z;
   auto kern = decode_pair16_kernel<S, ZS, ET>;
   cudaFuncAttributes fa;
@@ -417,7 +415,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const size_t cwsb = (size_t)((z * RS + 15) & ~15);
+  const size_t cwsb = (size_t)cw_block_bytes(z);
   const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>() +
                         15) & ~(size_t)15) + (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block
   e = ensure_dyn_smem((const void*)kern, smem);

@@ -25,9 +25,6 @@ cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStrea
   }
 }
 
-int spec_row_stride_bytes(int elem) {
-  return kRowStrideUnits * elem;
-}
 
 
 // Choose between the register-resident and the TMEM-resident message store.
@@ -86,7 +83,7 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   }();
   if (tmem_env == 0) return;
   const int regs_tm = QCB_TM_REG_BASE + (elem == 2 ? 6 : 5) * maxdeg;
-  const int smem_cw = (z * kRowStrideUnits * elem + 15) & ~15;
+  const int smem_cw = cw_block_bytes(z);
   int cols = 0;
   const int g = tmem_plan(z, ne, (regs_tm + 7) / 8 * 8, smem_cw, w, &cols);
   if (g <= 0) return;

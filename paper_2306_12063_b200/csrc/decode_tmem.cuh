@@ -175,7 +175,6 @@ template <class S, class A, int ZS, bool ET>
 __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>()))
     decode_tmem_kernel(const __grid_constant__ SpecArgs a) {
   using LT = LayeredTm<S, A, ZS>;
-  constexpr int RS = row_stride_bytes<A>();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[kLayMaxCw], s_done[kLayMaxCw], s_iters[kLayMaxCw];
   __shared__ int s_active;
@@ -191,11 +190,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   const int64_t cw0 = (int64_t)blockIdx.x * G;
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
   const bool act = g < ncw;
-  const uint32_t cws = (uint32_t)((Z * RS + 15) & ~15);
+  const uint32_t cws = (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  uint32_t b0 = sbase + (uint32_t)g * cws + (uint32_t)(r * RS), b1;
+  uint32_t b0 = sbase + (uint32_t)g * cws + (uint32_t)(r * kCellBytes), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
-  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * RS)));
+  asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * kCellBytes)));
 
   // ---- TMEM: one warp allocates a.tmem_cols columns for the CTA ----------------
   if (warp == 0) {
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   // ---- channel LLRs -> [cw][c][j] ------------------------------------------------
   static_assert(A::kElem == 4, "float32 cells");
   {
-    load_llrs_f32(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, Z, sbase, cws, RS);
+    load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   }
   uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
   float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
-  store_outputs_cell32(hard, a.hard_packed, post, ncw, N, Z, sbase, cws, RS,
+  store_outputs_cell32<io_cells8<ZS>()>(hard, a.hard_packed, post, ncw, N, sbase,
                        [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
                        [](uint32_t v) { return __uint_as_float(v); });
   // ---- release TMEM ------------------------------------------------------------------
@@ -310,10 +309,9 @@ inline int tmem_plan(int z, int ne, int regs_per_thread, int smem_per_cw, int64_
 
 template <class S, class A, int ZS, bool ET>
 inline cudaError_t launch_tmem(const SpecArgs& a, cudaStream_t s) {
-  constexpr int RS = row_stride_bytes<A>();
   const int z = ZS > 0 ? ZS : a.z;
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (size_t)a.pairs * ((z * RS + 15) & ~15);
+  const size_t smem = (size_t)a.pairs * cw_block_bytes(z);
   auto kern = decode_tmem_kernel<S, A, ZS, ET>;
   cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
@@ -328,9 +326,9 @@ inline cudaError_t launch_tmem(const SpecArgs& a, cudaStream_t s) {
     b.pairs = fa.maxThreadsPerBlock / z;
     if (b.pairs < 1) return cudaErrorLaunchOutOfResources;
     if (b.tmem_cols > 0) return cudaErrorLaunchOutOfResources;   // TMEM plan is per CTA shape
-    return launch_layered_fixed(kern, b, z, RS, s);
+    return launch_layered_fixed(kern, b, z, s);
   }
-  return launch_layered_fixed(kern, a, z, RS, s);
+  return launch_layered_fixed(kern, a, z, s);
 }
 
 
