@@ -27,6 +27,10 @@
 #pragma once
 #include "decode_layered.cuh"
 
+#ifndef QCB_P16_TAB_LATE
+#define QCB_P16_TAB_LATE 0
+#endif
+
 namespace qcb {
 
 __device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
@@ -120,8 +124,10 @@ struct Layered2 {
     tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ec, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
-    tab_fetch<S, ZS, TAB, T + 1>(tab, en);
+    if constexpr (!QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
     A::template row<D, (S::ID >= 12)>(p, o, nm + E0, K);   // anchor minima on the WiMAX structures
+    // late: the next tier's table entries are not live across the row update
+    if constexpr (QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       uint32_t v = o[k];
