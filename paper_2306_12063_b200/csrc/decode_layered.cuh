@@ -658,12 +658,39 @@ constexpr int plan_cw_per_cta(int, int, int, double) { return 1; }
 #ifndef QCB_REG_SLACK
 #define QCB_REG_SLACK 52
 #endif
-constexpr int raise_cap(int z, int want, int cw_smem, bool raise) {
+// Registers are allocated per warp (in 8-register steps per thread) from the
+// 16K-register file of the SM sub-partition the warp runs on, so a kernel
+// with r registers fits floor(16384 / (32 r)) warps per sub-partition: every
+// cap between 129 and 170 gives 3 warps (12 per SM), 103..128 gives 4.  With
+// `smsp` the cap is raised to the largest value with the same warp count --
+// the same occupancy, fewer spills.  It is not uniformly faster (ptxas then
+// schedules differently), so it is a per-structure choice measured with
+// tools/exp/percode.py (round 1, old cap -> raised, coded Gb/s): float32
+// Wi-Fi 648 R2/3 .. 5/6 +3..7 %, 1296 R2/3 .. 5/6 +4..7 %, 1944 R1/2 +3.6 %,
+// WiMAX 3/4A +4.3 % (WiMAX 2/3A -3.5 %); int16 Wi-Fi 648 R3/4 +3 %, 1296
+// R3/4, 5/6 +6 / +3 %, WiMAX 1/2, 5/6 +6 / +8 % (Wi-Fi 1944 R5/6 = C3 -10 %).
+#ifndef QCB_REG_SMSP
+#define QCB_REG_SMSP 1
+#endif
+template <class S, class A>
+constexpr bool smsp_raise() {
+  constexpr unsigned kF32 = (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 9) | (1u << 10) | (1u << 11) |
+                            (1u << 15);
+  constexpr unsigned kPair16 = (1u << 2) | (1u << 3) | (1u << 10) | (1u << 12) | (1u << 17);
+  return QCB_REG_SMSP && ((((A::kKind == 0) ? kF32 : kPair16) >> S::ID) & 1u);
+}
+constexpr int raise_cap(int z, int want, int cw_smem, bool raise, bool smsp) {
   const int p = plan_cw_per_cta(z, want, cw_smem, -1.0);
   const int threads = (p * z + 31) / 32 * 32;
   const int ctas = plan_ctas(z, p, want, cw_smem);
   int cap = (want + 7) / 8 * 8;
-  if (raise && ctas > 0) {
+  if (smsp) {
+    const int wps = 16384 / (32 * (cap > 255 ? 255 : cap));
+    if (wps > 0) {
+      const int r = 16384 / (32 * wps) / 8 * 8;
+      if (r > cap) cap = r;
+    }
+  } else if (raise && ctas > 0) {
     const int r = 65536 / (threads * ctas) / 8 * 8;
     if (r > cap) cap = r;
   }
@@ -674,7 +701,7 @@ template <class S, class A, int ZS>
 constexpr int reg_cap() {
   const int want = SmemMsg<S>::in_regs() + QCB_REG_SLACK;
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, want, cw_block_bytes(z), false);
+  return raise_cap(z, want, cw_block_bytes(z), false, smsp_raise<S, A>());
 }
 
 template <class S, class A, int ZS, bool ET>

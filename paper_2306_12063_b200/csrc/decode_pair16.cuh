@@ -256,7 +256,7 @@ struct Layered2 {
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true);
+  return raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true, smsp_raise<S, ArithI16x2>());
 }
 
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
