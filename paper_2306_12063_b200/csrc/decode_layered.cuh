@@ -142,6 +142,45 @@ __device__ __forceinline__ void loo_minima(const V (&a)[D], V (&ex)[D], Min mn, 
   }
 }
 
+// The same leave-one-out minima with every 3-term minimum handed to ptxas as
+// ONE inline-asm block (min3).  Composed from separate 2-input asm mins, the
+// compiler CSEs the shared inner terms (P[k-1] min a[k-1] feeds both P[k+1] and
+// ex[k]), after which ptxas cannot form VIMNMX3 and emits ~3D - 6 two-input
+// mins; as separate blocks every term becomes one VIMNMX3 (same issue cost as
+// a VIMNMX, measured: tools/exp/vmin3_bench.cu): 28 instead of 37 instructions
+// for D = 14.
+template <int D, class V, class Min, class Min3>
+__device__ __forceinline__ void loo_minima3(const V (&a)[D], V (&ex)[D], Min mn, Min3 mn3, V inf) {
+  static_assert(D >= 2, "row degree >= 2");
+  if constexpr (D == 2) {
+    ex[0] = mn(a[1], inf);
+    ex[1] = mn(a[0], inf);
+  } else if constexpr (D == 3) {
+    ex[0] = mn3(a[1], a[2], inf);
+    ex[1] = mn3(a[0], a[2], inf);
+    ex[2] = mn3(a[0], a[1], inf);
+  } else {
+    V P[D + 1], S[D + 1];
+    P[2] = mn3(a[0], a[1], inf);                          // P[k] = min a[0..k-1], k even
+#pragma unroll
+    for (int k = 4; k <= D - 1; k += 2) P[k] = mn3(P[k - 2], a[k - 2], a[k - 1]);
+    S[D - 3] = mn3(a[D - 2], a[D - 1], inf);              // S[k] = min a[k+1..D-1], D-1-k even
+#pragma unroll
+    for (int k = D - 5; k >= 0; k -= 2) S[k] = mn3(S[k + 2], a[k + 2], a[k + 1]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      V v;
+      if (k == 0) v = ((D - 1) % 2 == 0) ? S[0] : mn(S[1], a[1]);
+      else if (k == D - 1) v = (k % 2 == 0) ? P[k] : mn(P[k - 1], a[k - 1]);
+      else if (k == 1) v = ((D - 2) % 2 == 0) ? mn(a[0], S[1]) : mn3(a[0], S[2], a[2]);
+      else if (k == D - 2) v = (k % 2 == 0) ? mn(P[k], a[D - 1]) : mn3(P[k - 1], a[k - 1], a[D - 1]);
+      else if (k % 2 == 0) v = ((D - 1 - k) % 2 == 0) ? mn(P[k], S[k]) : mn3(P[k], S[k + 1], a[k + 1]);
+      else v = ((D - 1 - k) % 2 == 0) ? mn3(P[k - 1], a[k - 1], S[k]) : mn(mn3(P[k - 1], a[k - 1], S[k + 1]), a[k + 1]);
+      ex[k] = v;
+    }
+  }
+}
+
 struct RtK {              // runtime constants (kernel parameters)
   uint32_t one, sign, shr, neg1, lane1;   // lane1 = 0x00010001 (16x2 kernels)
 };

@@ -27,6 +27,9 @@
 #pragma once
 #include "decode_layered.cuh"
 
+#ifndef QCB_P16_MIN3
+#define QCB_P16_MIN3 2
+#endif
 #ifndef QCB_P16_TAB_LATE
 #define QCB_P16_TAB_LATE 0
 #endif
@@ -41,6 +44,12 @@ __device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) {
 }
 __device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) {
   uint32_t d; asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+// min of three in ONE asm block, so that ptxas forms VIMNMX3 (see loo_minima3)
+__device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("{\n\t.reg .b32 t;\n\tmin.s16x2 t, %1, %2;\n\tmin.s16x2 %0, t, %3;\n\t}" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
 }
 // lane sign masks: 0xFFFF in a lane whose bit 15 is set
 __device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
@@ -71,7 +80,10 @@ struct ArithI16x2 {
     for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
     if (D & 1) sx ^= d[D - 1];
     uint32_t exa[D];
-    if constexpr (ANCHOR) {
+    if constexpr (QCB_P16_MIN3 == 2 || (QCB_P16_MIN3 == 1 && ANCHOR)) {
+      loo_minima3<D>(a, exa, [](uint32_t x, uint32_t y) { return vmin2(x, y); },
+                     [](uint32_t x, uint32_t y, uint32_t z) { return vmin3(x, y, z); }, 0x7FFF7FFFu);
+    } else if constexpr (ANCHOR) {
       loo_minima<D>(a, exa, [](uint32_t x, uint32_t y) { return vmin2(x, y); }, 0x7FFF7FFFu);
     } else {
       // suffix / prefix chains step two edges at a time (VIMNMX3.S16x2)
