@@ -90,6 +90,17 @@ __device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// 3-input float min (PTX min.f32 with three sources -> FMNMX3): fminf
+// semantics, NaN inputs ignored unless all are NaN
+__device__ __forceinline__ float f_min3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+#ifndef QCB_F32_MIN3
+#define QCB_F32_MIN3 1
+#endif
+
 // packed float32x2 add/sub (FADD2: two IEEE float32 ops in one instruction)
 __device__ __forceinline__ void f_sub2(float a0, float a1, float b0, float b1, float& r0, float& r1) {
   asm("{\n\t.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
@@ -231,7 +242,17 @@ struct ArithF32 {
     // leave-one-out minima of |zz|
     // chains step two edges at a time through 3-input mins (FMNMX3), odd
     // entries hang off them: depth ~D/2 instead of D, same instruction count
-    float pre[D], suf[D], ex[D];
+    float ex[D];
+#if QCB_F32_MIN3
+    {
+      float az[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) az[k] = fabsf(zz[k]);      // |.| folds into FMNMX3 operand modifiers
+      loo_minima3<D>(az, ex, [](float x, float y) { return fminf(x, y); },
+                     [](float x, float y, float z) { return f_min3(x, y, z); }, f_inf());
+    }
+#else
+    float pre[D], suf[D];
     pre[1] = fabsf(zz[0]);
 #pragma unroll
     for (int k = 2; k < D; ++k) {
@@ -251,6 +272,7 @@ struct ArithF32 {
     ex[D - 1] = D == 2 ? fminf(pre[D - 1], f_inf()) : pre[D - 1];
 #pragma unroll
     for (int k = 1; k < D - 1; ++k) ex[k] = fminf(pre[k], suf[k]);
+#endif
     // pass 2 (_kernels.py:76-79): L_new = +-ex, sign = parity ^ sign(zz_k);
     // ex >= 0, so the sign is added to the bit pattern (IMAD, FMA pipe)
 #pragma unroll
