@@ -735,9 +735,13 @@ constexpr int plan_cw_per_cta(int, int, int, double) { return 1; }
 #endif
 template <class S, class A>
 constexpr bool smsp_raise() {
+#ifdef QCB_SMSP_F32                               // tuning experiments (both masks)
+  constexpr unsigned kF32 = QCB_SMSP_F32, kPair16 = QCB_SMSP_P16;
+#else
   constexpr unsigned kF32 = (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 9) | (1u << 10) | (1u << 11) |
                             (1u << 15);
   constexpr unsigned kPair16 = (1u << 2) | (1u << 3) | (1u << 10) | (1u << 12) | (1u << 17);
+#endif
   return QCB_REG_SMSP && ((((A::kKind == 0) ? kF32 : kPair16) >> S::ID) & 1u);
 }
 constexpr int raise_cap(int z, int want, int cw_smem, bool raise, bool smsp) {
