@@ -726,10 +726,11 @@ constexpr int plan_cw_per_cta(int, int, int, double) { return 1; }
 // `smsp` the cap is raised to the largest value with the same warp count --
 // the same occupancy, fewer spills.  It is not uniformly faster (ptxas then
 // schedules differently), so it is a per-structure choice measured with
-// tools/exp/percode.py (round 1, old cap -> raised, coded Gb/s): float32
-// Wi-Fi 648 R2/3 .. 5/6 +3..7 %, 1296 R2/3 .. 5/6 +4..7 %, 1944 R1/2 +3.6 %,
-// WiMAX 3/4A +4.3 % (WiMAX 2/3A -3.5 %); int16 Wi-Fi 648 R3/4 +3 %, 1296
-// R3/4, 5/6 +6 / +3 %, WiMAX 1/2, 5/6 +6 / +8 % (Wi-Fi 1944 R5/6 = C3 -10 %).
+// tools/exp/regmask_ab.sh (round 1, after the 3-input minima; none -> all
+// raised, coded Gb/s): float32 Wi-Fi 648 +4..8 %, 1296 +2..5 %, 1944 R1/2
+// +1.5 %, WiMAX 2/3A +1.7 % (Wi-Fi 1944 R2/3 -4 %); int16 Wi-Fi 648 +2..7 %,
+// 1296 R3/4, 5/6 +7 / +10 %, WiMAX 1/2, 5/6 +7 / +10 % (Wi-Fi 1944 R5/6 = C3
+// -5 %, 1296 R2/3 -4 %); unlisted structures are within +-1 % either way.
 #ifndef QCB_REG_SMSP
 #define QCB_REG_SMSP 1
 #endif
@@ -738,9 +739,8 @@ constexpr bool smsp_raise() {
 #ifdef QCB_SMSP_F32                               // tuning experiments (both masks)
   constexpr unsigned kF32 = QCB_SMSP_F32, kPair16 = QCB_SMSP_P16;
 #else
-  constexpr unsigned kF32 = (1u << 1) | (1u << 2) | (1u << 3) | (1u << 4) | (1u << 9) | (1u << 10) | (1u << 11) |
-                            (1u << 15);
-  constexpr unsigned kPair16 = (1u << 2) | (1u << 3) | (1u << 10) | (1u << 12) | (1u << 17);
+  constexpr unsigned kF32 = 0xFu | (1u << 4) | (0xFu << 8) | (1u << 13) | (1u << 15);
+  constexpr unsigned kPair16 = (1u << 2) | (1u << 3) | (0xFu << 8) | (1u << 12) | (1u << 17);
 #endif
   return QCB_REG_SMSP && ((((A::kKind == 0) ? kF32 : kPair16) >> S::ID) & 1u);
 }
