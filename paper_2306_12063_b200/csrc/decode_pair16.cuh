@@ -27,6 +27,9 @@
 #pragma once
 #include "decode_layered.cuh"
 
+#ifndef QCB_P16_XORSIGN
+#define QCB_P16_XORSIGN 0
+#endif
 #ifndef QCB_P16_MIN3
 #define QCB_P16_MIN3 2
 #endif
@@ -66,7 +69,7 @@ struct ArithI16x2 {
 
   // One row of D edges: posteriors p[] in, new posteriors o[] out, negated
   // messages nm[] updated in place (both codewords' lanes).
-  template <int D, bool ANCHOR = false>
+  template <int D, bool ANCHOR = false, bool XORSIGN = false>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* nm, const RtK& K) {
     static_assert(D >= 2, "row degree >= 2");
     uint32_t d[D], a[D];
@@ -108,9 +111,17 @@ struct ArithI16x2 {
     for (int k = 0; k < D; ++k) {
       const uint32_t ex = exa[k];
       const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
-      const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
-      o[k] = vadd2(d[k], (nex & m) | (ex & ~m));                   // post = zz + L_new
-      nm[k] = (ex & m) | (nex & ~m);                               // -L_new
+      if constexpr (XORSIGN) {
+        // L_new = (ex + m) ^ m: a lane with m = 0xFFFF gets ~(ex - 1) = -ex
+        // (wrapping: -(-32768) = -32768); the message's negation on the FMA pipe
+        const uint32_t ln = vadd2(ex, m) ^ m;
+        o[k] = vadd2(d[k], ln);                                    // post = zz + L_new
+        nm[k] = vadd2(imad(ln, K.neg1, K.neg1), K.lane1);          // -L_new
+      } else {
+        const uint32_t nex = vadd2(imad(ex, K.neg1, K.neg1), K.lane1);   // -ex (wrapping)
+        o[k] = vadd2(d[k], (nex & m) | (ex & ~m));                 // post = zz + L_new
+        nm[k] = (ex & m) | (nex & ~m);                             // -L_new
+      }
     }
   }
 };
@@ -137,7 +148,10 @@ struct Layered2 {
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
     if constexpr (!QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
-    A::template row<D, (S::ID >= 12)>(p, o, nm + E0, K);   // anchor minima on the WiMAX structures
+    // sign application: two selects, or (ex + m) ^ m with the message negated
+    // on the FMA pipe where measured faster (tools/exp/pc16_run.sh: Wi-Fi 1944
+    // R5/6 = C3 +2.8 %; WiMAX 1/2 -4.8 %, 3/4A -2 %; others within +-1 %)
+    A::template row<D, (S::ID >= 12), (QCB_P16_XORSIGN || S::ID == 7)>(p, o, nm + E0, K);
     // late: the next tier's table entries are not live across the row update
     if constexpr (QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
 #pragma unroll
