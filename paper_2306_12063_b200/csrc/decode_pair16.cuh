@@ -216,6 +216,12 @@ struct Layered2 {
   // stops once every lane in `need` is known to fail.  Returns this thread's
   // bits | the flag's (a set flag bit means some thread found that lane odd).
   static constexpr int kEtChunk = QCB_ET_CHUNKS > 0 ? (S::MB + QCB_ET_CHUNKS - 1) / QCB_ET_CHUNKS : 1;
+  // QCB_ET_FIRST > 0: a first group of that many tiers (a cheap reject of a
+  // codeword that has not converged), then all remaining tiers in one group
+  template <int T0>
+  static constexpr int et_len() {
+    return QCB_ET_FIRST > 0 ? (T0 == 0 ? QCB_ET_FIRST : S::MB - QCB_ET_FIRST) : kEtChunk;
+  }
   template <int T0, int... Is>
   __device__ __forceinline__ static uint32_t parity_group(const SpecArgs& a, int r, uint32_t b0, uint32_t b1,
                                                           uint32_t tab, std::integer_sequence<int, Is...>) {
@@ -269,9 +275,9 @@ struct Layered2 {
       return acc;
     } else {
       if (((acc | (uint32_t)*flag) & need) == need) return acc | ((uint32_t)*flag & need);
-      const uint32_t p = parity_group<T0>(a, r, b0, b1, tab, std::make_integer_sequence<int, kEtChunk>{}) & need;
+      const uint32_t p = parity_group<T0>(a, r, b0, b1, tab, std::make_integer_sequence<int, et_len<T0>()>{}) & need;
       if (p & ~acc) atomicOr((int*)flag, (int)p);
-      return parity_any<T0 + kEtChunk>(a, r, b0, b1, tab, flag, need, acc | p);
+      return parity_any<T0 + et_len<T0>()>(a, r, b0, b1, tab, flag, need, acc | p);
     }
   }
 };
