@@ -259,7 +259,9 @@ struct Layered2 {
       if (((acc | f_prev) & need) == need) return acc | (f_prev & need);
       return parity_pipe<T + 1>(a, r, b0, b1, tab, flag, need, acc, nxt, f);
     } else {
-      return acc | (lane_parity<T>(cur) & need) | (f_prev & need);
+      const uint32_t p = lane_parity<T>(cur) & need;
+      if (p & ~acc) atomicOr((int*)flag, (int)p);           // published like every other tier's bits
+      return acc | p | (f_prev & need);
     }
   }
   template <int T0>
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
   __shared__ int s_active;
-  __shared__ int s_odd;                         // early-exit syndrome lane bits (G == 1 with ET)
+  __shared__ int s_odd2[2];                     // early-exit syndrome lane bits, per sweep parity (G == 1 with ET)
 
   const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
-    if (tid == 0) s_odd = 0;
+    if (tid == 0) s_odd2[0] = s_odd2[1] = 0;
   }
   __syncthreads();
 
@@ -376,14 +378,22 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
       ++k;
 #if QCB_ET_EARLY_EXIT
+      // every odd lane bit a thread finds is published to this sweep's flag
+      // (parity_any), so one barrier makes the flag the CTA-wide OR; the flags
+      // alternate between sweeps, and the other one -- last read before this
+      // sweep's tier barriers -- is cleared for the next sweep
+      volatile int* fl = &s_odd2[k & 1];
       const uint32_t need = (done_a ? 0u : 1u) | (done_b ? 0u : 2u);
-      const uint32_t par = act ? L::template parity_any<0>(a, rs, b0, b1, tab, &s_odd, need) : 0u;
+      if (act) L::template parity_any<0>(a, rs, b0, b1, tab, fl, need);
+      __syncthreads();
+      const uint32_t all = (uint32_t)*fl;
+      if (tid == 0) s_odd2[(k + 1) & 1] = 0;
+      const int fa = (int)(all & 1u), fb = (int)((all >> 1) & 1u);
 #else
       const uint32_t par = act ? L::parity_all(a, rs, b0, b1, tab, tiers) : 0u;
-#endif
       const int fa = __syncthreads_or((int)(par & 1u));
       const int fb = __syncthreads_or((int)(par & 2u));
-      if (tid == 0) s_odd = 0;
+#endif
       uint32_t newly = 0;
       if (!done_a) { it_a = k; fail_a = fa; done_a = !fa; if (done_a) newly |= 0x0000FFFFu; }
       if (!done_b) { it_b = k; fail_b = fb; done_b = !fb; if (done_b) newly |= 0xFFFF0000u; }
