@@ -809,7 +809,17 @@ template <class S, class A, int ZS>
 constexpr int reg_cap() {
   const int want = SmemMsg<S>::in_regs() + QCB_REG_SLACK;
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, want, cw_block_bytes(z), false, smsp_raise<S, A>());
+  const int cap = raise_cap(z, want, cw_block_bytes(z), false, smsp_raise<S, A>());
+  // the other direction: 128 registers = 4 warps per sub-partition (5 CTAs of
+  // 3 warps instead of 4), paid for with spills.  Measured per structure
+  // (tools/exp/cap128_ab.sh, Gb/s): WiMAX 2/3A 75.8 -> 79.3, 3/4A 66.7 -> 69.0,
+  // Wi-Fi 1944 R3/4 56.3 -> 57.3; every other float32 code loses up to 6 %.
+#ifdef QCB_F32_CAP_MAX                                 // tuning experiments
+  constexpr int kMax = QCB_F32_CAP_MAX;
+#else
+  constexpr int kMax = ((((1u << 6) | (1u << 13) | (1u << 15)) >> S::ID) & 1u) ? 128 : 255;
+#endif
+  return cap > kMax ? kMax : cap;
 }
 
 template <class S, class A, int ZS, bool ET>
