@@ -290,7 +290,18 @@ struct Layered2 {
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
   const int z = ZS > 0 ? ZS : 96;
-  return raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true, smsp_raise<S, ArithI16x2>());
+  const int cap = raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true, smsp_raise<S, ArithI16x2>());
+  // 128 registers = 4 warps per sub-partition, paid for with spills; measured
+  // per structure (tools/exp/pc16_ab.sh, Gb/s): Wi-Fi 1296 R1/2 75.1 -> 78.9,
+  // 1944 R1/2 71.3 -> 74.1, R2/3 66.3 -> 67.1, R5/6 (C3) 65.4 -> 68.6, WiMAX
+  // 2/3A 86.8 -> 88.4, 2/3B 86.4 -> 90.2; the other int16 codes lose 1..11 %.
+#ifdef QCB_P16_CAP_MAX                                 // tuning experiments
+  constexpr int kMax = QCB_P16_CAP_MAX;
+#else
+  constexpr int kMax =
+      ((((1u << 0) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 13) | (1u << 14)) >> S::ID) & 1u) ? 128 : 255;
+#endif
+  return cap > kMax ? kMax : cap;
 }
 
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
