@@ -366,8 +366,14 @@ constexpr bool use_addr_tab() {
 #else
   constexpr unsigned kF32 = (1u << 5) | (1u << 6) | (1u << 14) | (1u << 15) | (1u << 16);
 #endif
-  constexpr unsigned kPair16 = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 6) | (1u << 8) | (1u << 9) |
-                               (0x3Fu << 12);
+#ifdef QCB_P16_TAB_MASK
+  constexpr unsigned kPair16 = QCB_P16_TAB_MASK;   // tuning experiments
+#else
+  // re-measured after the 3-input minima and register caps (tools/exp/tab_ab.sh):
+  // Wi-Fi 648 R1/2 drops its table (+2.7 %), 648 R3/4 and 1296 R2/3 take one
+  // (+6.9 / +1.8 %); float32 unchanged (all / none within 1 % of this policy)
+  constexpr unsigned kPair16 = 0x7u | (0x7u << 4) | (0x3u << 9) | (0x3Fu << 12);
+#endif
   return QCB_ADDR_TAB && ((A::kKind == 0 && ((kF32 >> S::ID) & 1u)) || (A::kKind == 2 && ((kPair16 >> S::ID) & 1u)));
 }
 
