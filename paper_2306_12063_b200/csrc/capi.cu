@@ -367,7 +367,10 @@ int qc_decode_i16(qc_code_t code, const int16_t* llr, int64_t w, int32_t max_ite
 namespace {
 
 // Per-device side streams for the grouped launch (created once, never freed).
-constexpr int kGroupStreams = 8;
+#ifndef QCB_GROUP_STREAMS
+#define QCB_GROUP_STREAMS 8
+#endif
+constexpr int kGroupStreams = QCB_GROUP_STREAMS;
 cudaStream_t* group_streams(int device, cudaError_t* err) {
   static std::mutex m;
   static std::map<int, std::vector<cudaStream_t>> all;
