@@ -788,7 +788,7 @@ constexpr bool smsp_raise() {
 #ifdef QCB_SMSP_F32                               // tuning experiments (both masks)
   constexpr unsigned kF32 = QCB_SMSP_F32, kPair16 = QCB_SMSP_P16;
 #else
-  constexpr unsigned kF32 = 0xFu | (1u << 4) | (0xFu << 8) | (1u << 13) | (1u << 15);
+  constexpr unsigned kF32 = 0xFu | (1u << 4) | (1u << 7) | (0xFu << 8) | (1u << 13) | (1u << 15) | (1u << 17);
   constexpr unsigned kPair16 = (1u << 2) | (1u << 3) | (0xFu << 8) | (1u << 12) | (1u << 17);
 #endif
   return QCB_REG_SMSP && ((((A::kKind == 0) ? kF32 : kPair16) >> S::ID) & 1u);

@@ -59,7 +59,7 @@ bool spec_is_scaled(int structure_id, int z, const int32_t* ent_e, int ne) {
   return scaled;
 }
 
-void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
+void spec_plan(int structure_id, int elem, int z, int native, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
                int32_t* pair16) {
   int ne = 0, maxdeg = 0;
   *pair16 = 0;
@@ -92,7 +92,17 @@ void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta
   // WiMAX 1152 R5/6 34.7 / 43.7); degree 22 loses (Wi-Fi 648 R5/6 39.7 / 35.4,
   // Wi-Fi 1296 R5/6 43.8 / 33.5) and so do the low-degree codes (5-6 %):
   // TMEM reads (64 B/clk/SM) only pay where the register kernel is starved
-  const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20;
+  // Re-measured at the end of round 1 (3-input minima, register caps at the
+  // sub-partition boundary): the register kernel now wins on the native
+  // degree-20 codes (Wi-Fi 1944 R5/6 59.6 vs 55.7, WiMAX 2304 R5/6 70.0 vs
+  // 66.0 Gb/s, tools/exp/deg20_ab.sh); TMEM stays preferred for the scaled
+  // (runtime-Z) degree-20 codes with Z >= 40, where it measured ahead
+  // (tools/exp/tmem_scaled_ab.sh: WiMAX 1152 R5/6 54.4 vs 52.5, 1728 R5/6
+  // 51.7 vs 45.5; 576 R5/6 48.4 vs 51.7 keeps the register kernel).
+#ifndef QCB_TMEM_SCALED
+#define QCB_TMEM_SCALED 1
+#endif
+  const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20 && QCB_TMEM_SCALED && !native && z >= 40;
   if (tmem_env == 1 || prefer) {
     *cw_per_cta = g;
     *tmem_cols = cols;

@@ -47,7 +47,7 @@ struct SpecArgs {
 
 // returns cudaErrorInvalidValue if no specialised kernel exists for (structure, elem)
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s);
-void spec_plan(int structure_id, int elem, int z, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
+void spec_plan(int structure_id, int elem, int z, int native, int64_t w, int32_t* cw_per_cta, int32_t* tmem_cols,
                int32_t* pair16);
 // true when (z, tier-major shifts) equal the structure's native Z0 / SHIFT0 tables
 bool spec_is_native(int structure_id, int z, const int32_t* ent_e, int ne);

@@ -516,3 +516,34 @@ def test_bit_granular_encoder_pipeline_many_tiles(std, n, rate):
     want = P.pack_bits(P.encode_array(P.make_plan(mm), bits))
     got = P.encode_bits(mm, torch.from_numpy(P.pack_bits(bits)).cuda()).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+def test_tmem_message_kernel_matches_oracle():
+    """The TMEM-resident-message float32 kernel (csrc/decode_tmem.cuh), forced with
+    QCB_TMEM=1 in a fresh process (the choice is read once per process), on the
+    degree-20 codes and a low-degree one, fixed iterations and early termination."""
+    import subprocess
+    import sys
+    script = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2306_12063_b200 as P
+from oracle import oracle as O
+from tests._util import noisy_llrs
+for i, code in enumerate([("wifi", 1944, "5/6"), ("wimax", 2304, "5/6"), ("wimax", 1152, "5/6"), ("wimax", 2304, "1/2")]):
+    mm = P.get_model_matrix(*code)
+    llr, _, _ = noisy_llrs(mm, 37, 2.5 + mm.rate.fraction, seed=500 + i)
+    for early in (False, True):
+        cfg = P.DecoderConfig(max_iterations=6, early_termination=early)
+        hard, it, conv, post = [t.cpu().numpy() for t in P.decode_batch(mm, torch.from_numpy(llr).cuda(), cfg, posteriors=True)]
+        oh, oi, oc, op = O.decode_batch(P.expand(mm), llr, 6, early, workers=4, want_post=True)
+        assert np.array_equal(hard, oh) and np.array_equal(it, oi) and np.array_equal(conv, oc), code
+        assert np.array_equal(post, op, equal_nan=True), code
+print("ok")
+'''
+    import os
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, QCB_TMEM="1")
+    res = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout + res.stderr
