@@ -28,7 +28,7 @@
 #include "decode_layered.cuh"
 
 #ifndef QCB_P16_XORSIGN
-#define QCB_P16_XORSIGN 0
+#define QCB_P16_XORSIGN 0   // 0: per-structure choice, 1: everywhere, 2: nowhere (experiments)
 #endif
 #ifndef QCB_P16_MIN3
 #define QCB_P16_MIN3 2
@@ -151,7 +151,7 @@ struct Layered2 {
     // sign application: two selects, or (ex + m) ^ m with the message negated
     // on the FMA pipe where measured faster (tools/exp/pc16_run.sh: Wi-Fi 1944
     // R5/6 = C3 +2.8 %; WiMAX 1/2 -4.8 %, 3/4A -2 %; others within +-1 %)
-    A::template row<D, (S::ID >= 12), (QCB_P16_XORSIGN || S::ID == 7)>(p, o, nm + E0, K);
+    A::template row<D, (S::ID >= 12), (QCB_P16_XORSIGN == 1 || (QCB_P16_XORSIGN == 0 && S::ID == 7))>(p, o, nm + E0, K);
     // late: the next tier's table entries are not live across the row update
     if constexpr (QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
 #pragma unroll
