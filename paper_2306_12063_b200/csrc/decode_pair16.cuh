@@ -18,10 +18,11 @@
 // about evenly between the half-rate ALU and FMA-heavy pipes:
 //   pass 1  d = p + nm                                   (VIADD.16x2)
 //           a = max(d, ~d + 0x10001) = |d| (wrapping)    (IMAD, VIADD, VIMNMX)
-//   minima  ex_k = min_{j != k} a_j (prefix / suffix)    (VIMNMX)
+//   minima  ex_k = min_{j != k} a_j (prefix / suffix anchors, loo_minima3: VIMNMX3)
 //   pass 2  m    = lane sign mask of d ^ parity          (LOP3, PRMT)
 //           nex  = ~ex + 0x10001 = -ex                   (IMAD, VIADD)
 //           post = d + (m ? nex : ex), nm = m ? ex : nex (LOP3, VIADD, LOP3)
+//           (Wi-Fi 1944 R5/6: L_new = (ex + m) ^ m, nm = -L_new, measured faster)
 // Shared memory layout, addressing and tier schedule are the float32
 // kernel's (4-byte cells, decode_layered.cuh).
 #pragma once
