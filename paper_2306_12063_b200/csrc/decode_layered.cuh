@@ -556,6 +556,20 @@ __device__ __forceinline__ void sts128f(uint32_t a, float x, float y, float z, f
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
 
+// Tier barrier.  A one-warp CTA (native Z <= 32: Wi-Fi 648, one codeword per
+// CTA, forced at launch) needs no CTA barrier between tiers: __syncwarp
+// orders the warp's shared-memory stores before its lanes' next loads.
+#ifndef QCB_WARP_SYNC
+#define QCB_WARP_SYNC 1
+#endif
+template <int ZS>
+constexpr bool one_warp_cta() { return QCB_WARP_SYNC && ZS > 0 && ZS <= 32; }
+template <int ZS>
+__device__ __forceinline__ void tier_sync() {
+  if constexpr (one_warp_cta<ZS>()) __syncwarp();
+  else __syncthreads();
+}
+
 template <class S, class A, int ZS>
 struct Layered {
   using Val = typename A::Val;
@@ -641,12 +655,12 @@ struct Layered {
       ((work ? tier<Ts>(a, K, r, b0, b1, tab, mbase, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
                         (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
              : void(),
-        __syncthreads()), ...);
+        tier_sync<ZS>()), ...);
     } else {
       (void)work;
       ((tier<Ts>(a, K, r, b0, b1, tab, mbase, msg, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
                  (Ts & 1) ? ea : eb),
-        __syncthreads()), ...);
+        tier_sync<ZS>()), ...);
     }
   }
 
@@ -986,6 +1000,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
   b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
+  if constexpr (one_warp_cta<ZS>()) b.pairs = 1;            // tier_sync is a warp barrier
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   return launch_layered_fixed(kern, b, z, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),

@@ -197,12 +197,12 @@ struct Layered2 {
       ((work ? tier<Ts, true>(a, K, r, b0, b1, tab, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
                               (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
              : void(),
-        __syncthreads()), ...);
+        tier_sync<ZS>()), ...);
     } else {
       (void)work; (void)keep;
       ((tier<Ts, false>(a, K, r, b0, b1, tab, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
                         (Ts & 1) ? ea : eb),
-        __syncthreads()), ...);
+        tier_sync<ZS>()), ...);
     }
   }
 
@@ -472,6 +472,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
   b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4);
+  if constexpr (one_warp_cta<ZS>()) b.pairs = 1;            // tier_sync is a warp barrier
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
