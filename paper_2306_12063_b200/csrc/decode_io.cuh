@@ -18,7 +18,12 @@
 
 namespace qcb {
 
-constexpr int kIoUnroll = 4;
+// units in flight per thread; measured (C5 / C3 / C2 Gb/s): 2: 80.1 / 84.4 /
+// 88.0, 4: 82.6 / 84.9 / 88.4, 8: 81.1 / 81.4 / 88.3
+#ifndef QCB_IO_UNROLL
+#define QCB_IO_UNROLL 4
+#endif
+constexpr int kIoUnroll = QCB_IO_UNROLL;
 // float32 I/O unit: 8 cells (two 16-byte groups, swizzled) or 4 cells (one
 // group).  Measured (C2 / C1 / C4 Gb/s): 4 + 4: 85.3 / 29.6 / 61.4;
 // 8 + 8: 84.7 / 30.6 / 62.0 -- so the kernels pick 8-cell units for the
