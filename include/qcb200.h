@@ -78,10 +78,12 @@ int qc_decode_i16(qc_code_t code, const int16_t* llr, int64_t w, int32_t max_ite
                   int32_t early_term, uint8_t* hard, int32_t hard_packed, int32_t* iters,
                   uint8_t* conv, int16_t* post_out, void* cuda_stream);
 
-/* ---- mixed-code batch: one job per code.  Every job is validated first; the
- * jobs then fork from cuda_stream onto side streams and join back (stream
- * ordered, graph-capturable), so the codes decode concurrently.  Set
- * QCB_GROUPED_SERIAL=1 to queue them one after another on cuda_stream. */
+/* ---- mixed-code batch: one job per code.  Every job is validated first
+ * (arguments, and the generic kernel's shared-memory fit); the jobs then fork
+ * from cuda_stream onto side streams and join back (stream ordered,
+ * graph-capturable), so the codes decode concurrently.  If a CUDA launch
+ * fails part-way the call returns its error and the outputs are unspecified.
+ * Set QCB_GROUPED_SERIAL=1 to queue the jobs one after another on cuda_stream. */
 typedef struct {
   qc_code_t code;
   const void* llr;   /* device, w x n float32 or int16 (per call) */
@@ -99,7 +101,11 @@ int qc_decode_grouped_i16(const qc_decode_job_t* jobs, int32_t n_jobs, int32_t m
 /* ---- host-buffer drop-ins for _kernels.decode_batch_f32 / _i16 -----------
  * Arguments in the reference order.  llrs/hard are w x n row-major host
  * arrays; hard is unpacked (one byte per bit).  Blocks until the outputs are
- * written.  Uses the current CUDA device. */
+ * written.  Uses the current CUDA device.  The block streams through the
+ * device in ~32 MB chunks on three streams; page-locked caller buffers are
+ * copied directly by DMA, pageable ones (plain numpy, as decode_block passes
+ * them) through pinned staging slots filled / drained by a host copy pool
+ * (QCB_COPY_THREADS threads) while the previous chunks transfer and decode. */
 int qc_decode_batch_f32_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,
                              int64_t n_edges, int32_t mb, int32_t z, const float* llrs, int64_t w,
                              int64_t n, int32_t max_iters, int32_t early_term, uint8_t* hard,

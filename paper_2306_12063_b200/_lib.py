@@ -147,3 +147,63 @@ class Code:
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
             self._h = None
+
+
+class DeviceCall:
+    """Context for one stream-ordered library call on CUDA tensors.
+
+    The C side launches on whatever device is current, so the call runs under
+    `torch.cuda.device(device)`; `stream` (default: that device's current
+    stream) must live on the same device.  Tensors handed to the kernel that
+    the caching allocator could recycle while it still runs on a side stream
+    (contiguous temporaries, fresh outputs) are registered with `keep()`:
+    when the call's stream is not the current stream, they are marked as used
+    on it (`record_stream`) so their memory is not reused early.
+
+        with DeviceCall(t.device, stream, t, *others) as call:
+            out = torch.empty(...); call.keep(out)
+            check(lib().qc_x(..., call.stream_ptr))
+    """
+
+    def __init__(self, device, stream=None, *tensors):
+        import torch
+        dev = torch.device(device)
+        if dev.type != "cuda":
+            raise ValueError(f"expected a CUDA device, got {dev}")
+        if dev.index is None:                  # "cuda" = the current device
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        for t in tensors:
+            if t is not None and t.device != self.device:
+                raise ValueError(f"all tensors of one call must be on {self.device}, got {t.device}")
+        self._stream = stream
+        self._keep = [t for t in tensors if t is not None]
+
+    def __enter__(self):
+        import torch
+        self._guard = torch.cuda.device(self.device)
+        self._guard.__enter__()
+        cur = torch.cuda.current_stream(self.device)
+        self.stream = self._stream if self._stream is not None else cur
+        if self.stream.device != self.device:
+            self._guard.__exit__(None, None, None)
+            raise ValueError(f"stream is on {self.stream.device}, tensors on {self.device}")
+        self._side = self.stream != cur
+        self.stream_ptr = C.c_void_p(self.stream.cuda_stream)
+        return self
+
+    def keep(self, *tensors):
+        for t in tensors:
+            if t is not None:
+                if t.device != self.device:
+                    raise ValueError(f"all tensors of one call must be on {self.device}, got {t.device}")
+                self._keep.append(t)
+
+    def __exit__(self, et, ev, tb):
+        try:
+            if et is None and self._side:
+                for t in self._keep:
+                    t.record_stream(self.stream)
+        finally:
+            self._guard.__exit__(et, ev, tb)
+        return False

@@ -25,7 +25,6 @@ exactly where the reference's sequential loop would.
 
 from __future__ import annotations
 
-import ctypes as C
 import math
 from dataclasses import dataclass, field, replace
 
@@ -156,33 +155,31 @@ class ThroughputReport:
 
 # --- device operations (CUDA torch tensors, stream ordered) ----------------------
 
-def _stream(dev, stream):
-    import torch
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    return C.c_void_p(s.cuda_stream)
-
-
 def encode_array_device(code, info_bits, stream=None):
     """Bit-per-byte encoder on the device (encoder.encode_array, any Z):
     (W, K) uint8 CUDA tensor -> (W, N) uint8."""
     import torch
     c = code_handle(code)
     k = c.n - c.mb * c.z
-    t = info_bits.contiguous()
-    if t.dim() != 2 or t.shape[1] != k or t.dtype != torch.uint8 or not t.is_cuda:
+    if info_bits.dim() != 2 or info_bits.shape[1] != k or info_bits.dtype != torch.uint8 or not info_bits.is_cuda:
         raise SizeMismatch(f"info bits must be a (W, {k}) uint8 CUDA tensor")
-    out = torch.empty((t.shape[0], c.n), dtype=torch.uint8, device=t.device)
-    _lib.check(_lib.lib().qc_encode_array(c.handle, _lib.ptr(t), t.shape[0], _lib.ptr(out),
-                                          _stream(t.device, stream)), "encode_array")
+    with _lib.DeviceCall(info_bits.device, stream) as call:
+        t = info_bits.contiguous()
+        out = torch.empty((t.shape[0], c.n), dtype=torch.uint8, device=t.device)
+        call.keep(t, out)
+        _lib.check(_lib.lib().qc_encode_array(c.handle, _lib.ptr(t), t.shape[0], _lib.ptr(out), call.stream_ptr),
+                   "encode_array")
     return out
 
 
 def frames_info_device(seed: int, point: int, frame0: int, w: int, k: int, device, stream=None):
     """Info bits of frames [frame0, frame0+w) from the device Philox stream."""
     import torch
-    out = torch.empty((w, k), dtype=torch.uint8, device=device)
-    _lib.check(_lib.lib().qc_frames_info(seed & (2**64 - 1), point, frame0, w, k, _lib.ptr(out),
-                                         _stream(out.device, stream)), "frames_info")
+    with _lib.DeviceCall(device, stream) as call:
+        out = torch.empty((w, k), dtype=torch.uint8, device=device)
+        call.keep(out)
+        _lib.check(_lib.lib().qc_frames_info(seed & (2**64 - 1), point, frame0, w, k, _lib.ptr(out),
+                                             call.stream_ptr), "frames_info")
     return out
 
 
@@ -196,18 +193,20 @@ def channel_llr_device(cw_bits, sigma2: float, arithmetic: Arithmetic = Arithmet
     import torch
     if sigma2 <= 0:
         raise DivByZeroSigma(f"sigma2 = {sigma2}")
-    t = cw_bits.contiguous()
-    w, n = t.shape
     fixed = arithmetic is Arithmetic.Fixed16
-    out = torch.empty((w, n), dtype=torch.int16 if fixed else torch.float32, device=t.device)
-    nz = None
-    if noise is not None:
-        nz = noise.contiguous()
-        if nz.shape != t.shape or nz.dtype != torch.float64:
-            raise SizeMismatch("noise must be a float64 tensor shaped like the codeword bits")
-    _lib.check(_lib.lib().qc_channel_llr(_lib.ptr(t), w, n, float(sigma2), _lib.ptr(nz), seed & (2**64 - 1),
-                                         point, frame0, q_b if fixed else 0, float(l_clip), _lib.ptr(out),
-                                         _stream(t.device, stream)), "channel_llr")
+    with _lib.DeviceCall(cw_bits.device, stream, noise) as call:
+        t = cw_bits.contiguous()
+        w, n = t.shape
+        out = torch.empty((w, n), dtype=torch.int16 if fixed else torch.float32, device=t.device)
+        nz = None
+        if noise is not None:
+            nz = noise.contiguous()
+            if nz.shape != t.shape or nz.dtype != torch.float64:
+                raise SizeMismatch("noise must be a float64 tensor shaped like the codeword bits")
+        call.keep(t, out, nz)
+        _lib.check(_lib.lib().qc_channel_llr(_lib.ptr(t), w, n, float(sigma2), _lib.ptr(nz), seed & (2**64 - 1),
+                                             point, frame0, q_b if fixed else 0, float(l_clip), _lib.ptr(out),
+                                             call.stream_ptr), "channel_llr")
     return out
 
 
@@ -216,12 +215,14 @@ def quantize_llr_device(x, q_b: int = 10, l_clip: float = 24.0, stream=None):
     import torch
     if not 1 <= q_b <= 14:
         raise ValueError("q_b must stay in [1, 14]")
-    t = x.contiguous()
-    if t.dtype != torch.float32:
+    if x.dtype != torch.float32:
         raise SizeMismatch("quantize_llr_device wants float32")
-    out = torch.empty(t.shape, dtype=torch.int16, device=t.device)
-    _lib.check(_lib.lib().qc_quantize_llr(_lib.ptr(t), t.numel(), q_b, float(l_clip), _lib.ptr(out),
-                                          _stream(t.device, stream)), "quantize_llr")
+    with _lib.DeviceCall(x.device, stream) as call:
+        t = x.contiguous()
+        out = torch.empty(t.shape, dtype=torch.int16, device=t.device)
+        call.keep(t, out)
+        _lib.check(_lib.lib().qc_quantize_llr(_lib.ptr(t), t.numel(), q_b, float(l_clip), _lib.ptr(out),
+                                              call.stream_ptr), "quantize_llr")
     return out
 
 
@@ -232,11 +233,12 @@ def count_errors_device(hard, info_bits, iters, k: int, *, batch: int = BATCH_FR
     import torch
     w = info_bits.shape[0]
     n = n if n is not None else (hard.shape[1] if not hard_packed else hard.shape[1] * 8)
-    sums = torch.empty(((w + batch - 1) // batch, 3), dtype=torch.int64, device=info_bits.device)
-    _lib.check(_lib.lib().qc_count_errors(_lib.ptr(hard.contiguous()), 1 if hard_packed else 0,
-                                          _lib.ptr(info_bits.contiguous()), _lib.ptr(iters.contiguous()),
-                                          w, n, k, batch, _lib.ptr(sums), _stream(info_bits.device, stream)),
-               "count_errors")
+    with _lib.DeviceCall(info_bits.device, stream, hard, iters) as call:
+        h, inf, it = hard.contiguous(), info_bits.contiguous(), iters.contiguous()
+        sums = torch.empty(((w + batch - 1) // batch, 3), dtype=torch.int64, device=info_bits.device)
+        call.keep(h, inf, it, sums)
+        _lib.check(_lib.lib().qc_count_errors(_lib.ptr(h), 1 if hard_packed else 0, _lib.ptr(inf), _lib.ptr(it),
+                                              w, n, k, batch, _lib.ptr(sums), call.stream_ptr), "count_errors")
     return sums
 
 

@@ -15,6 +15,8 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <condition_variable>
+#include <thread>
 #include <vector>
 
 #include "../../include/qcb200.h"
@@ -58,17 +60,30 @@ struct qc_code_s {
   std::mutex mu;
   std::map<int, DeviceTables> dev;   // generic decoder tables per device
 
-  const int32_t* tables(int device, cudaError_t* err) {
+  std::vector<int32_t> host_tables;  // tier_start | ent_j | ent_e (the upload source, kept alive)
+
+  // Generic-kernel tables on `device`: uploaded once (qc_code_create does it
+  // eagerly for the current device), stream ordered on `stream` otherwise.
+  // Refused inside a CUDA graph capture: cudaMalloc is not capturable.
+  const int32_t* tables(int device, cudaStream_t stream, cudaError_t* err, bool* capturing) {
     std::lock_guard<std::mutex> lk(mu);
+    *capturing = false;
     auto it = dev.find(device);
     if (it != dev.end()) return it->second.d;
-    std::vector<int32_t> host(tier_start);
-    host.insert(host.end(), ent_j.begin(), ent_j.end());
-    host.insert(host.end(), ent_e.begin(), ent_e.end());
-    int32_t* d = nullptr;
-    *err = cudaMalloc(&d, host.size() * sizeof(int32_t));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    *err = cudaStreamIsCapturing(stream, &cs);
     if (*err != cudaSuccess) return nullptr;
-    *err = cudaMemcpy(d, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (cs != cudaStreamCaptureStatusNone) { *capturing = true; return nullptr; }
+    if (host_tables.empty()) {
+      host_tables = tier_start;
+      host_tables.insert(host_tables.end(), ent_j.begin(), ent_j.end());
+      host_tables.insert(host_tables.end(), ent_e.begin(), ent_e.end());
+    }
+    int32_t* d = nullptr;
+    *err = cudaMalloc(&d, host_tables.size() * sizeof(int32_t));
+    if (*err != cudaSuccess) return nullptr;
+    *err = cudaMemcpyAsync(d, host_tables.data(), host_tables.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           stream);
     if (*err != cudaSuccess) { cudaFree(d); return nullptr; }
     dev[device].d = d;
     return d;
@@ -126,6 +141,14 @@ int build_code(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Codewords per CTA of the generic kernel, 0 if one codeword does not fit in shared memory.
+int generic_cw_per_cta(const qc_code_s* c, int elem) {
+  int g = std::max(1, std::min(64, 256 / std::max(1, c->z)));
+  const size_t limit = 160 * 1024;
+  while (g > 1 && generic_smem_bytes(g, c->n, c->mb * c->z, elem) > limit) --g;
+  return generic_smem_bytes(g, c->n, c->mb * c->z, elem) > 227 * 1024 ? 0 : g;
+}
+
 template <typename T>
 int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32_t early_term,
                   uint8_t* hard, int32_t hard_packed, int32_t* iters, uint8_t* conv, T* post,
@@ -158,7 +181,11 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
   int device = 0;
   e = cudaGetDevice(&device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const int32_t* tab = c->tables(device, &e);
+  bool capturing = false;
+  const int32_t* tab = c->tables(device, stream, &e, &capturing);
+  if (capturing)
+    return fail(QC_EINVAL, "first use of a generic code on device %d inside a CUDA graph capture: decode once "
+                "before capturing (qc_code_create uploads the tables for the current device)", device);
   if (!tab) return cuda_fail(e, "uploading code tables");
   GenericArgs a;
   memset(&a, 0, sizeof a);
@@ -166,24 +193,106 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
   a.w = w; a.n = c->n; a.z = c->z; a.mb = c->mb; a.max_iters = max_iters;
   a.early_term = early_term ? 1 : 0; a.hard_packed = hard_packed ? 1 : 0;
   a.tier_start = tab; a.ent_j = tab + c->mb + 1; a.ent_e = tab + c->mb + 1 + c->ne;
-  int g = std::max(1, std::min(64, 256 / std::max(1, c->z)));
-  const size_t limit = 160 * 1024;
-  while (g > 1 && generic_smem_bytes(g, c->n, c->mb * c->z, elem) > limit) --g;
-  if (generic_smem_bytes(g, c->n, c->mb * c->z, elem) > 227 * 1024)
-    return fail(QC_EUNSUPPORTED, "one codeword (N=%d) does not fit in shared memory", c->n);
+  const int g = generic_cw_per_cta(c, elem);
+  if (g < 1) return fail(QC_EUNSUPPORTED, "one codeword (N=%d) does not fit in shared memory", c->n);
   a.cw_per_cta = g;
   e = launch_generic(a, elem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "decode (generic kernel)");
   return QC_OK;
 }
 
-// ---- host-buffer path: cached codes and device workspace --------------------
+// ---- host-buffer path: cached codes, device workspace, pinned staging ----------
+
+// A small persistent pool of host threads for the staging copies between the
+// caller's (pageable) arrays and the pinned slots: one memcpy thread moves
+// ~6-10 GB/s, a PCIe 5 x16 link ~50 GB/s per direction.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();   // never destroyed: threads outlive static teardown
+    return *p;
+  }
+  struct Task { void* dst; const void* src; size_t n; };
+  // Run every task split into ~equal pieces over the pool; returns when all are done.
+  void run(const std::vector<Task>& tasks) {
+    size_t total = 0;
+    for (const Task& t : tasks) total += t.n;
+    if (total == 0) return;
+    std::vector<Task> pieces;
+    const size_t piece = std::max<size_t>(1 << 20, (total + 4 * nthreads_ - 1) / (4 * nthreads_));
+    for (const Task& t : tasks)
+      for (size_t o = 0; o < t.n; o += piece)
+        pieces.push_back({static_cast<char*>(t.dst) + o, static_cast<const char*>(t.src) + o,
+                          std::min(piece, t.n - o)});
+    if (nthreads_ <= 1 || pieces.size() == 1) {
+      for (const Task& p : pieces) memcpy(p.dst, p.src, p.n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    work_ = &pieces;
+    next_ = 0;
+    left_ = pieces.size();
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    drain();                                  // the caller works too
+    lk.lock();
+    done_cv_.wait(lk, [&] { return left_ == 0; });
+    work_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    const char* v = getenv("QCB_COPY_THREADS");
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    nthreads_ = v ? std::max(1, atoi(v)) : (int)std::min(16u, std::max(1u, hw / 2));
+    for (int i = 1; i < nthreads_; ++i) std::thread([this] { loop(); }).detach();
+  }
+  void drain() {
+    for (;;) {
+      size_t i;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!work_ || next_ >= work_->size()) return;
+        i = next_++;
+      }
+      const Task& p = (*work_)[i];
+      memcpy(p.dst, p.src, p.n);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--left_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      drain();
+    }
+  }
+  int nthreads_ = 1;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::vector<Task>* work_ = nullptr;
+  size_t next_ = 0, left_ = 0;
+  uint64_t gen_ = 0;
+};
+
+constexpr int kHostSlots = 3;
+
+struct HostSlot {
+  cudaStream_t st = nullptr;
+  cudaEvent_t done = nullptr;
+  void* dev = nullptr;  size_t dev_cap = 0;    // llr | hard | iters | conv
+  void* pin = nullptr;  size_t pin_cap = 0;    // pinned staging: llr | hard | iters | conv
+};
 
 struct HostCtx {
   std::mutex mu;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  void* buf[2] = {nullptr, nullptr};
-  size_t cap[2] = {0, 0};
+  HostSlot slot[kHostSlots];
   std::map<std::vector<int32_t>, qc_code_t> codes;
 };
 
@@ -194,6 +303,13 @@ HostCtx& host_ctx(int device) {
   auto& p = ctxs[device];
   if (!p) p.reset(new HostCtx());
   return *p;
+}
+
+// true when [p, p+n) is page-locked (cudaHostAlloc / cudaHostRegister / torch pin_memory)
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeHost;
 }
 
 int csr_to_shifts(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx, int64_t n_edges,
@@ -258,48 +374,104 @@ int decode_host(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_
   } else {
     code = it->second;
   }
-  for (int i = 0; i < 2; ++i)
-    if (!ctx.st[i]) {
-      e = cudaStreamCreateWithFlags(&ctx.st[i], cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-    }
-  // chunked, double-buffered: H2D(i+1) overlaps decode(i) (two streams)
+  // Caller buffers that are already page-locked are copied by the DMA engines
+  // directly; pageable ones (numpy, as decode_block passes them,
+  // decoder.py:235-246) go through pinned staging slots filled and drained by
+  // a host copy pool, so the copies of chunk i+1 / i-2 overlap chunk i's
+  // transfer and decode.
+  const bool direct = is_pinned(llrs) && is_pinned(hard) && is_pinned(iters) && is_pinned(conv);
   static const int64_t chunk_bytes = [] {
     const char* v = getenv("QCB_HOST_CHUNK_MB");
     return (int64_t)(v ? atoi(v) : 32) << 20;   // tools/exp/e2e_chunk.sh: 16-32 MB best
   }();
   const int64_t chunk = std::min<int64_t>(w, std::max<int64_t>(512, chunk_bytes / (n * (int64_t)sizeof(T))));
   const size_t llr_b = (size_t)chunk * n * sizeof(T), hard_b = (size_t)chunk * n;
-  const size_t need = llr_b + hard_b + (size_t)chunk * 8 + 256;
-  for (int i = 0; i < 2; ++i)
-    if (ctx.cap[i] < need) {
-      if (ctx.buf[i]) cudaFree(ctx.buf[i]);
-      ctx.buf[i] = nullptr; ctx.cap[i] = 0;
-      e = cudaMalloc(&ctx.buf[i], need);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc workspace");
-      ctx.cap[i] = need;
+  const size_t it_off = (llr_b + hard_b + 127) & ~(size_t)127;
+  const size_t need = it_off + (size_t)chunk * 5 + 256;
+  const size_t pin_it = (hard_b + 127) & ~(size_t)127, pin_need = llr_b + pin_it + (size_t)chunk * 5 + 256;
+  for (HostSlot& s : ctx.slot) {
+    if (!s.st) {
+      e = cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "host path streams");
     }
-  for (int64_t c0 = 0, ci = 0; c0 < w; c0 += chunk, ++ci) {
-    const int b = (int)(ci & 1);
+    if (s.dev_cap < need) {
+      if (s.dev) cudaFree(s.dev);
+      s.dev = nullptr; s.dev_cap = 0;
+      e = cudaMalloc(&s.dev, need);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc workspace");
+      s.dev_cap = need;
+    }
+    if (!direct && s.pin_cap < pin_need) {
+      if (s.pin) cudaFreeHost(s.pin);
+      s.pin = nullptr; s.pin_cap = 0;
+      e = cudaHostAlloc(&s.pin, pin_need, cudaHostAllocDefault);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc staging");
+      s.pin_cap = pin_need;
+    }
+  }
+  CopyPool& pool = CopyPool::get();
+  int64_t pending[kHostSlots] = {-1, -1, -1};   // first codeword of the chunk a slot holds (staged path)
+  auto copy_out = [&](int b, std::vector<CopyPool::Task>& tasks) {
+    const int64_t c0 = pending[b];
+    if (c0 < 0) return;
     const int64_t cw = std::min(chunk, w - c0);
-    char* base = static_cast<char*>(ctx.buf[b]);
+    char* p = static_cast<char*>(ctx.slot[b].pin);
+    tasks.push_back({hard + c0 * n, p + llr_b, (size_t)cw * n});
+    tasks.push_back({iters + c0, p + llr_b + pin_it, (size_t)cw * 4});
+    tasks.push_back({conv + c0, p + llr_b + pin_it + (size_t)chunk * 4, (size_t)cw});
+    pending[b] = -1;
+  };
+  for (int64_t c0 = 0, ci = 0; c0 < w; c0 += chunk, ++ci) {
+    const int b = (int)(ci % kHostSlots);
+    HostSlot& s = ctx.slot[b];
+    const int64_t cw = std::min(chunk, w - c0);
+    char* base = static_cast<char*>(s.dev);
     T* d_llr = reinterpret_cast<T*>(base);
     uint8_t* d_hard = reinterpret_cast<uint8_t*>(base + llr_b);
-    int32_t* d_it = reinterpret_cast<int32_t*>(base + llr_b + hard_b + 128 - ((llr_b + hard_b) & 127));
+    int32_t* d_it = reinterpret_cast<int32_t*>(base + it_off);
     uint8_t* d_conv = reinterpret_cast<uint8_t*>(d_it + chunk);
-    cudaStream_t s = ctx.st[b];
-    e = cudaMemcpyAsync(d_llr, llrs + c0 * n, (size_t)cw * n * sizeof(T), cudaMemcpyHostToDevice, s);
+    const T* src = llrs + c0 * n;
+    uint8_t* o_hard = hard + c0 * n;
+    int32_t* o_it = iters + c0;
+    uint8_t* o_conv = conv + c0;
+    if (!direct) {
+      // the slot's previous chunk (c0 - 3 chunks) must have landed before its
+      // staging buffer is reused; drain it and stage this chunk in one pass
+      e = cudaEventSynchronize(s.done);
+      if (e != cudaSuccess) return cuda_fail(e, "decode (host path)");
+      std::vector<CopyPool::Task> tasks;
+      copy_out(b, tasks);
+      char* p = static_cast<char*>(s.pin);
+      tasks.push_back({p, src, (size_t)cw * n * sizeof(T)});
+      pool.run(tasks);
+      src = reinterpret_cast<const T*>(p);
+      o_hard = reinterpret_cast<uint8_t*>(p + llr_b);
+      o_it = reinterpret_cast<int32_t*>(p + llr_b + pin_it);
+      o_conv = reinterpret_cast<uint8_t*>(p + llr_b + pin_it + (size_t)chunk * 4);
+      pending[b] = c0;
+    }
+    e = cudaMemcpyAsync(d_llr, src, (size_t)cw * n * sizeof(T), cudaMemcpyHostToDevice, s.st);
     if (e != cudaSuccess) return cuda_fail(e, "H2D llr");
-    rc = decode_device<T>(code, d_llr, cw, max_iters, early_term, d_hard, 0, d_it, d_conv, nullptr, s);
+    rc = decode_device<T>(code, d_llr, cw, max_iters, early_term, d_hard, 0, d_it, d_conv, nullptr, s.st);
     if (rc) return rc;
-    e = cudaMemcpyAsync(hard + c0 * n, d_hard, (size_t)cw * n, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(iters + c0, d_it, (size_t)cw * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(conv + c0, d_conv, (size_t)cw, cudaMemcpyDeviceToHost, s);
+    e = cudaMemcpyAsync(o_hard, d_hard, (size_t)cw * n, cudaMemcpyDeviceToHost, s.st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(o_it, d_it, (size_t)cw * 4, cudaMemcpyDeviceToHost, s.st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(o_conv, d_conv, (size_t)cw, cudaMemcpyDeviceToHost, s.st);
+    if (e == cudaSuccess) e = cudaEventRecord(s.done, s.st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H outputs");
   }
-  for (int i = 0; i < 2; ++i) {
-    e = cudaStreamSynchronize(ctx.st[i]);
+  // drain the slots in chunk order
+  const int64_t nchunks = (w + chunk - 1) / chunk;
+  for (int64_t ci = std::max<int64_t>(0, nchunks - kHostSlots); ci < nchunks; ++ci) {
+    const int b = (int)(ci % kHostSlots);
+    e = cudaEventSynchronize(ctx.slot[b].done);
     if (e != cudaSuccess) return cuda_fail(e, "decode (host path)");
+    if (!direct) {
+      std::vector<CopyPool::Task> tasks;
+      copy_out(b, tasks);
+      pool.run(tasks);
+    }
   }
   return QC_OK;
 }
@@ -312,7 +484,20 @@ int qc_version(void) { return 110; }
 const char* qc_last_error(void) { return g_err.c_str(); }
 
 int qc_code_create(int32_t mb, int32_t nb, int32_t z, const int32_t* shifts, qc_code_t* out) {
-  return build_code(mb, nb, z, shifts, out);
+  const int rc = build_code(mb, nb, z, shifts, out);
+  if (rc || (*out)->structure >= 0) return rc;
+  // generic code: upload its tables for the current device now, so the first
+  // decode is free of allocations (and capturable).  No device: skip quietly.
+  int device = 0, count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0 || cudaGetDevice(&device) != cudaSuccess) {
+    cudaGetLastError();
+    return rc;
+  }
+  cudaError_t e = cudaSuccess;
+  bool capturing = false;
+  if ((*out)->tables(device, nullptr, &e, &capturing) && e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+  if (e != cudaSuccess) cudaGetLastError();   // decode retries (and reports) the upload
+  return rc;
 }
 
 int qc_code_from_csr(const int32_t* row_ptr, int64_t row_ptr_len, const int32_t* col_idx,
@@ -393,10 +578,16 @@ int validate_job(const qc_decode_job_t& j, int32_t max_iters) {
   if (!j.code) return fail(QC_EINVAL, "code is NULL");
   if (j.w < 0 || max_iters < 0) return fail(QC_EINVAL, "w=%lld max_iters=%d", (long long)j.w, max_iters);
   if (j.w > 0 && (!j.llr || !j.hard || !j.iters || !j.conv)) return fail(QC_EINVAL, "NULL buffer");
+  if (j.w > (int64_t)1 << 40) return fail(QC_EINVAL, "batch too large");
+  // the one data-independent failure decode_device can report, checked before any job is queued
+  if (j.code->structure < 0 && generic_cw_per_cta(j.code, (int)sizeof(T)) < 1)
+    return fail(QC_EUNSUPPORTED, "one codeword (N=%d) does not fit in shared memory", j.code->n);
   return QC_OK;
 }
 
-// Mixed-code batch.  Every job is validated before any work is queued; the
+// Mixed-code batch.  Every job is validated before any work is queued (argument
+// checks and the generic kernel's shared-memory fit; a CUDA launch failure can
+// still stop the call part-way, and then the outputs are unspecified); the
 // jobs then fork from the caller's stream onto per-device side streams
 // (event record / wait, so the call stays stream-ordered and can be captured
 // into a CUDA graph) and join back, so the codes' kernels run concurrently:

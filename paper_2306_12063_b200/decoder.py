@@ -308,26 +308,27 @@ def decode_batch(code, llrs, cfg: DecoderConfig | None = None, *, hard_packed: b
     import torch
     t = llrs
     _check_llrs(t, c, cfg)
-    t = t.contiguous()
-    w = t.shape[0]
-    dev = t.device
-    if out is None:
-        hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=dev)
-        iters = torch.empty(w, dtype=torch.int32, device=dev)
-        conv = torch.empty(w, dtype=torch.uint8, device=dev)
-        post = torch.empty_like(t) if posteriors else None
-    else:
-        hard, iters, conv = out[:3]
-        _check_out(hard, iters, conv, w, c.n, hard_packed, dev)
-        post = out[3] if posteriors else None
-        if post is not None and (post.shape != t.shape or post.dtype != t.dtype or post.device != dev
-                                 or not post.is_contiguous()):
-            raise SizeMismatch(f"out post: need contiguous {t.dtype} {tuple(t.shape)} on {dev}")
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    fn = _lib.lib().qc_decode_f32 if cfg.arithmetic is Arithmetic.Float32 else _lib.lib().qc_decode_i16
-    _lib.check(fn(c.handle, _lib.ptr(t), w, cfg.max_iterations, 1 if cfg.early_termination else 0,
-                  _lib.ptr(hard), 1 if hard_packed else 0, _lib.ptr(iters), _lib.ptr(conv),
-                  _lib.ptr(post), C.c_void_p(s.cuda_stream)), "decode_batch")
+    with _lib.DeviceCall(t.device, stream) as call:
+        t = t.contiguous()
+        w = t.shape[0]
+        dev = t.device
+        if out is None:
+            hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=dev)
+            iters = torch.empty(w, dtype=torch.int32, device=dev)
+            conv = torch.empty(w, dtype=torch.uint8, device=dev)
+            post = torch.empty_like(t) if posteriors else None
+        else:
+            hard, iters, conv = out[:3]
+            _check_out(hard, iters, conv, w, c.n, hard_packed, dev)
+            post = out[3] if posteriors else None
+            if post is not None and (post.shape != t.shape or post.dtype != t.dtype or post.device != dev
+                                     or not post.is_contiguous()):
+                raise SizeMismatch(f"out post: need contiguous {t.dtype} {tuple(t.shape)} on {dev}")
+        call.keep(t, hard, iters, conv, post)
+        fn = _lib.lib().qc_decode_f32 if cfg.arithmetic is Arithmetic.Float32 else _lib.lib().qc_decode_i16
+        _lib.check(fn(c.handle, _lib.ptr(t), w, cfg.max_iterations, 1 if cfg.early_termination else 0,
+                      _lib.ptr(hard), 1 if hard_packed else 0, _lib.ptr(iters), _lib.ptr(conv),
+                      _lib.ptr(post), call.stream_ptr), "decode_batch")
     return (hard, iters, conv, post) if posteriors else (hard, iters, conv)
 
 
@@ -343,26 +344,32 @@ def decode_grouped(jobs, cfg: DecoderConfig | None = None, *, hard_packed: bool 
         raise ValueError("out must hold one (hard, iters, conv) triple per job")
     outs, arr = [], (_lib.DecodeJob * len(jobs))()
     keep = []
-    for i, (code, t) in enumerate(jobs):
-        c = code_handle(code)
-        _check_llrs(t, c, cfg)
-        t = t.contiguous()
-        w = t.shape[0]
-        if out is not None:
-            hard, iters, conv = out[i]
-            _check_out(hard, iters, conv, w, c.n, hard_packed, t.device)
-        else:
-            hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=t.device)
-            iters = torch.empty(w, dtype=torch.int32, device=t.device)
-            conv = torch.empty(w, dtype=torch.uint8, device=t.device)
-        arr[i] = _lib.DecodeJob(c.handle.value, t.data_ptr(), w, hard.data_ptr(), iters.data_ptr(),
-                                conv.data_ptr(), None)
-        outs.append((hard, iters, conv))
-        keep.append((c, t))
-    s = stream if stream is not None else torch.cuda.current_stream()
-    fn = (_lib.lib().qc_decode_grouped_f32 if cfg.arithmetic is Arithmetic.Float32
-          else _lib.lib().qc_decode_grouped_i16)
-    _lib.check(fn(C.cast(arr, C.c_void_p), len(jobs), cfg.max_iterations,
-                  1 if cfg.early_termination else 0, 1 if hard_packed else 0,
-                  C.c_void_p(s.cuda_stream)), "decode_grouped")
+    if not jobs:
+        return outs
+    dev = jobs[0][1].device
+    with _lib.DeviceCall(dev, stream) as call:
+        for i, (code, t) in enumerate(jobs):
+            c = code_handle(code)
+            _check_llrs(t, c, cfg)
+            if t.device != dev:
+                raise ValueError(f"decode_grouped: job {i} is on {t.device}, job 0 on {dev}")
+            t = t.contiguous()
+            w = t.shape[0]
+            if out is not None:
+                hard, iters, conv = out[i]
+                _check_out(hard, iters, conv, w, c.n, hard_packed, t.device)
+            else:
+                hard = torch.empty((w, (c.n + 7) // 8 if hard_packed else c.n), dtype=torch.uint8, device=dev)
+                iters = torch.empty(w, dtype=torch.int32, device=dev)
+                conv = torch.empty(w, dtype=torch.uint8, device=dev)
+            arr[i] = _lib.DecodeJob(c.handle.value, t.data_ptr(), w, hard.data_ptr(), iters.data_ptr(),
+                                    conv.data_ptr(), None)
+            outs.append((hard, iters, conv))
+            keep.append((c, t))
+            call.keep(t, hard, iters, conv)
+        fn = (_lib.lib().qc_decode_grouped_f32 if cfg.arithmetic is Arithmetic.Float32
+              else _lib.lib().qc_decode_grouped_i16)
+        _lib.check(fn(C.cast(arr, C.c_void_p), len(jobs), cfg.max_iterations,
+                      1 if cfg.early_termination else 0, 1 if hard_packed else 0,
+                      call.stream_ptr), "decode_grouped")
     return outs

@@ -15,7 +15,6 @@
 
 from __future__ import annotations
 
-import ctypes as C
 import os
 import struct
 
@@ -92,11 +91,12 @@ def pack_records_device(hard_packed, iters, conv, n: int, stream=None):
     """(W, ceil(N/8)+2) uint8 CUDA tensor of CLI decode records."""
     import torch
     w = iters.shape[0]
-    out = torch.empty((w, (n + 7) // 8 + 2), dtype=torch.uint8, device=iters.device)
-    s = stream if stream is not None else torch.cuda.current_stream(iters.device)
-    _lib.check(_lib.lib().qc_pack_records(_lib.ptr(hard_packed.contiguous()), _lib.ptr(iters.contiguous()),
-                                          _lib.ptr(conv.contiguous()), w, n, _lib.ptr(out),
-                                          C.c_void_p(s.cuda_stream)), "pack_records")
+    with _lib.DeviceCall(iters.device, stream, hard_packed, conv) as call:
+        hp, it, cv = hard_packed.contiguous(), iters.contiguous(), conv.contiguous()
+        out = torch.empty((w, (n + 7) // 8 + 2), dtype=torch.uint8, device=iters.device)
+        call.keep(hp, it, cv, out)
+        _lib.check(_lib.lib().qc_pack_records(_lib.ptr(hp), _lib.ptr(it), _lib.ptr(cv), w, n, _lib.ptr(out),
+                                              call.stream_ptr), "pack_records")
     return out
 
 

@@ -13,10 +13,13 @@ seeded uniform info bits, systematic encoding, BPSK (0 -> +1), AWGN with
 sigma^2 = 1 / (2 R 10^(EbN0/10)), LLR = 2y/sigma^2 in float64, then float32 or
 quantize_llr(q_b=10).  No public dataset is involved.
 
-To build BASELINE-sized batches quickly, `device_llrs` encodes a seeded pool of
-codewords on the host (numpy, exact reference encoder) and tiles it over the
-batch while drawing fresh Gaussian noise for every codeword on the GPU
-(torch Philox, seeded), so every LLR in the batch is distinct.  Decoding
+BASELINE-sized batches are generated on the device by `shard_llrs`, keyed by
+the GLOBAL frame index of the job: frame f of code ci gets its info bits and
+its AWGN samples from the counter-based Philox streams of the device channel
+(`qc_frames_info` / `qc_channel_llr`, keyed by (seed, ci, f)), is encoded by
+the device `encode_array`, and quantised exactly like `quantize_llr`.  A rank
+that owns frames [lo, hi) therefore holds exactly the rows [lo, hi) of the
+one-GPU batch, so hard decisions are comparable across GPU counts.  Decoding
 runs a fixed number of iterations, so the work does not depend on the data.
 """
 
@@ -99,30 +102,35 @@ def host_llrs(mm, w: int, ebn0_db: float, seed, fixed: bool):
     return (quantize_llr(llr).values if fixed else llr.astype(np.float32)), info
 
 
-def device_llrs(mm, w: int, ebn0_db: float, seed: int, fixed: bool, device, pool: int = 4096,
-                chunk: int = 32768):
-    """(W, N) LLR tensor on `device`: tiled host-encoded codeword pool + fresh device noise.
+def frame_range(wl: Workload, rank: int, world: int) -> tuple[int, int]:
+    """Global frames [lo, hi) of each code that `rank` decodes: its contiguous
+    shard of the job total (strong scaling, C5) or its own block of W frames
+    (weak scaling: rank r takes frames [r W, (r+1) W))."""
+    if wl.strong:
+        from .shard import shard_range
+        return shard_range(wl.w_per_code, rank, world)
+    return rank * wl.w_per_code, (rank + 1) * wl.w_per_code
 
-    Returns (llr tensor, codeword pool (P, N) uint8 tensor); codeword i of the
-    batch carries pool row i % P.
-    """
+
+def shard_info(wl: Workload, ci: int, lo: int, hi: int, device):
+    """Info bits (hi-lo, K) of global frames [lo, hi) of code ci (device Philox stream)."""
+    from .channel import frames_info_device
+    mm = wl.model_matrices()[ci]
+    return frames_info_device(wl.seed, ci, lo, hi - lo, mm.k, device)
+
+
+def shard_llrs(wl: Workload, ci: int, lo: int, hi: int, device, chunk: int = 1 << 16):
+    """(hi-lo, N) channel LLRs of global frames [lo, hi) of code ci, generated on
+    `device`: Philox info bits -> encode_array -> BPSK/AWGN (Philox noise keyed
+    by frame) -> float32 or quantize_llr(q_b=10).  Identical rows for a frame
+    whichever rank / shard generates it."""
     import torch
-    rng = np.random.default_rng([seed, 0])
-    p = min(pool, w) if w > 0 else 1
-    info = rng.integers(0, 2, size=(p, mm.k), dtype=np.uint8)
-    cw = torch.from_numpy(encode_array(make_plan(mm), info)).to(device)
-    s2 = sigma2(ebn0_db, mm.rate.fraction)
-    out = torch.empty((w, mm.n), dtype=torch.int16 if fixed else torch.float32, device=device)
-    g = torch.Generator(device=device).manual_seed(int(seed) * 1_000_003 + 17)
-    sym = (1.0 - 2.0 * cw.to(torch.float64))
-    lim = 1023.0
-    for c0 in range(0, w, chunk):
-        c1 = min(w, c0 + chunk)
-        idx = torch.arange(c0, c1, device=device) % p
-        noise = torch.randn((c1 - c0, mm.n), dtype=torch.float64, device=device, generator=g)
-        llr = (2.0 / s2) * (sym[idx] + math.sqrt(s2) * noise)
-        if fixed:
-            out[c0:c1] = torch.clamp(torch.round(llr * (lim / 24.0)), -lim, lim).to(torch.int16)
-        else:
-            out[c0:c1] = llr.to(torch.float32)
-    return out, cw
+    from .channel import channel_llr_device, encode_array_device
+    mm = wl.model_matrices()[ci]
+    s2 = sigma2(wl.ebn0_db, mm.rate.fraction)
+    out = torch.empty((hi - lo, mm.n), dtype=torch.int16 if wl.fixed else torch.float32, device=device)
+    for f0 in range(lo, hi, chunk):
+        f1 = min(hi, f0 + chunk)
+        cw = encode_array_device(mm, shard_info(wl, ci, f0, f1, device))
+        out[f0 - lo:f1 - lo] = channel_llr_device(cw, s2, wl.arithmetic, seed=wl.seed, point=ci, frame0=f0)
+    return out

@@ -59,3 +59,20 @@ def have_gpu() -> bool:
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+def acceptance_case(fixed: bool):
+    """The reference's decoder-oracle acceptance case
+    (/root/reference/pkg/tests/test_acceptance.py:139-156): WiMAX 576 R1/2,
+    1000 frames at 1.8 dB, seed 1004, 10 iterations with early termination.
+    Returns (h, llr values, hard, iters, conv); the LLRs are regenerated with the
+    reference recipe and checked against the fixture's SHA-256."""
+    import hashlib
+    z = np.load(GOLDEN / "acceptance_decoder_oracle.npz")
+    mm = CB.get_model_matrix("wimax", 576, "1/2")
+    vals, _, _ = noisy_llrs(mm, int(z["frames"]), float(z["ebn0_db"]), int(z["seed"]), fixed)
+    tag = "i16" if fixed else "f32"
+    assert hashlib.sha256(vals.tobytes()).digest() == z[f"llr_sha256_{tag}"].tobytes(), \
+        "LLR recipe drifted from the reference's (numpy generator / encoder / quantizer)"
+    hard = np.unpackbits(z[f"hard_packed_{tag}"], axis=-1, count=mm.n)
+    return CB.expand(mm), vals, hard, z[f"iters_{tag}"], z[f"conv_{tag}"]

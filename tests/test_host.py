@@ -188,3 +188,15 @@ def test_channel_abi_validates_before_touching_the_device():
     assert L.qc_quantize_llr(None, 0, 6, 1.0, None, None) == 0
     assert L.qc_pack_records(None, None, None, 0, 96, None, None) == 0
     assert L.qc_frames_info(1, 0, 0, 0, 48, None, None) == 0
+
+
+def test_device_call_refuses_non_cuda_devices():
+    """_lib.DeviceCall guards every library call: CUDA device only, and every
+    tensor of one call on that device (calls run on the tensors'
+    device, not whatever device happens to be current)."""
+    import torch
+    from paper_2306_12063_b200 import _lib
+    with pytest.raises(ValueError):
+        _lib.DeviceCall("cpu")
+    with pytest.raises(ValueError):
+        _lib.DeviceCall("cuda:0", None, torch.zeros(2))

@@ -68,3 +68,13 @@ def test_oracle_encoder_matches_reference(golden_dir):
         assert np.array_equal(got, z[key]), key
         checked += 1
     assert checked >= 20
+
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_oracle_matches_reference_acceptance_case(fixed):
+    """test_acceptance.py:139-156 (decoder-oracle): 1000 noisy frames per
+    arithmetic, hard bits / iterations / converged equal to the reference's."""
+    from tests._util import acceptance_case
+    h, llr, hard, iters, conv = acceptance_case(fixed)
+    oh, oi, oc = O.decode_batch(h, llr, 10, True, workers=4)
+    assert np.array_equal(oh, hard) and np.array_equal(oi, iters) and np.array_equal(oc, conv)

@@ -21,8 +21,17 @@ encode_packed.npz   reference `encode_packed` on seeded info words for
                     byte-aligned WiMAX codes, several word sizes.
 kat.npz             known answers: degree-3 row by hand (test_decoder.py:74-91),
                     quantizer points (test_decoder.py:274-289).
+acceptance_decoder_oracle.npz
+                    the reference's decoder-oracle acceptance case
+                    (pkg/tests/test_acceptance.py:139-156): WiMAX 576 R1/2,
+                    1000 frames at 1.8 dB, seed 1004, default DecoderConfig
+                    (10 iterations, early termination), Fixed16 and Float32;
+                    decode_block outputs (checked here against the explicit-
+                    message `_reference.ref_decode`, as that test does) plus the
+                    SHA-256 of the LLR block, which the tests regenerate with
+                    the same numpy recipe instead of storing 3 MB of LLRs.
 
-Usage:  python tools/make_golden.py
+Usage:  python tools/make_golden.py [kat|encode|special|decode|acceptance ...]
 """
 
 from __future__ import annotations
@@ -216,9 +225,30 @@ def make_kat():
     print("kat", st.posterior, ste.posterior, ste.min1)
 
 
+def make_acceptance():
+    import hashlib
+    mm = R.get_model_matrix(R.Standard.Wimax, 576, R.Rate.R12)
+    h = R.expand(mm)
+    arrs = {}
+    for arith, fixed in ((R.Arithmetic.Fixed16, True), (R.Arithmetic.Float32, False)):
+        vals, _, _ = noisy(mm, 1000, 1.8, 1004, fixed)
+        hard, iters, conv = ref_decode(h, vals, arith, 10, True)
+        for w in range(vals.shape[0]):     # the reference test's own oracle comparison
+            eh, ei, ec = RR.ref_decode(h, vals[w])
+            assert np.array_equal(hard[w], eh) and iters[w] == ei and bool(conv[w]) == bool(ec), w
+        tag = "i16" if fixed else "f32"
+        arrs[f"llr_sha256_{tag}"] = np.frombuffer(hashlib.sha256(vals.tobytes()).digest(), np.uint8)
+        arrs[f"hard_packed_{tag}"] = np.packbits(hard, axis=-1)
+        arrs[f"iters_{tag}"] = iters
+        arrs[f"conv_{tag}"] = conv
+    np.savez_compressed(OUT / "acceptance_decoder_oracle.npz", standard="wimax", n_bits=576, rate="1/2",
+                        frames=1000, ebn0_db=1.8, seed=1004, max_iters=10, early_term=1, **arrs)
+    print("acceptance: 1000 frames x 2 arithmetics equal to _reference.ref_decode")
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    make_kat()
-    make_encode()
-    make_special()
-    make_decode()
+    steps = {"kat": make_kat, "encode": make_encode, "special": make_special, "decode": make_decode,
+             "acceptance": make_acceptance}
+    for name in (sys.argv[1:] or list(steps)):
+        steps[name]()
