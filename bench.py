@@ -85,6 +85,8 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/check)")
     ap.add_argument("--no-encode", action="store_true", help="C5: skip the packed-encoder measurement")
     ap.add_argument("--no-graph", action="store_true", help="launch each step directly (no CUDA graph)")
+    ap.add_argument("--codewords", type=int, default=None,
+                    help="tests only: override the config's codewords per code (job total for C5)")
     return ap.parse_args()
 
 
@@ -403,12 +405,19 @@ def run_ours(args, wl):
     rank, local, world = dist_env()
     if world != args.gpus:
         raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    # QCB_BENCH_BACKEND=gloo: test hook that runs N ranks on fewer GPUs (ranks
+    # share a device round-robin; the decode kernels never wait on each other)
+    backend = os.environ.get("QCB_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        else:
+            dist.init_process_group(backend, init_method="env://")
     import paper_2306_12063_b200 as P
     from paper_2306_12063_b200 import _lib, shard
     from paper_2306_12063_b200.workloads import frame_range, shard_info, shard_llrs
@@ -700,6 +709,9 @@ def main():
         raise SystemExit(rc)
     from paper_2306_12063_b200.workloads import WORKLOADS
     wl = WORKLOADS[args.config]
+    if args.codewords is not None:
+        from dataclasses import replace
+        wl = replace(wl, w_per_code=args.codewords)
     if args.impl == "reference":
         run_reference(args, wl)
     else:

@@ -20,7 +20,7 @@
  * decoder.init_state + tier_update (decoder.py:94-149), which the golden
  * fixtures in tests/golden/ were generated from.
  *
- * Build: oracle/Makefile  (gcc -O2 -ffp-contract=off; no -ffast-math).
+ * Build: oracle/Makefile  (gcc -O3 -ffp-contract=off -fno-fast-math).
  */
 #include <math.h>
 #include <pthread.h>

@@ -15,10 +15,12 @@
 //    barrier between them (layered schedule); the Z rows of a tier touch
 //    disjoint columns, so running them concurrently equals the reference's
 //    row loop;
-//  * posteriors live in shared memory as [c][j] (c = position inside the
-//    circulant, j = block column, rows padded to 25 columns); the cyclic
-//    shift of edge (j, e) is the indexed shared-memory read at
-//    ((r + e) mod Z) * 25 + j -- no expanded H anywhere.  For the 18 native
+//  * posteriors live in shared memory in the codeword's own bit order: cell
+//    (c, j) -- bit n = j Z + c, c = position inside the circulant, j = block
+//    column -- at byte 4 n (the layout of the codeword's LLR row in HBM, so
+//    prologue and epilogue are streaming 16-byte copies); the cyclic shift of
+//    edge (j, e) is the indexed shared-memory read of cell ((r + e) mod Z, j)
+//    -- no expanded H anywhere.  For the 18 native
 //    codes Z and the shifts are compile-time constants; scaled WiMAX codes
 //    take them from the kernel parameter block; the per-edge base select is
 //    kept in registers or in a per-thread shared-memory address table,

@@ -26,7 +26,10 @@
 // Shared memory layout, addressing and tier schedule are the float32
 // kernel's (4-byte cells, decode_layered.cuh).
 #pragma once
+#include <mutex>
+
 #include "decode_layered.cuh"
+#include "decode_tmem.cuh"
 
 #ifndef QCB_P16_XORSIGN
 #define QCB_P16_XORSIGN 0   // 0: per-structure choice, 1: everywhere, 2: nowhere (experiments)
@@ -38,7 +41,57 @@
 #define QCB_P16_TAB_LATE 0
 #endif
 
+// Native-Z kernels: address table in global memory (read through L1) instead
+// of shared memory.  Measured on C5 (round 2, tools/exp/ab_r02_tmem.sh): 68.8
+// vs 82.5 Gb/s -- LDG latency on every tier's prefetch costs more than the
+// freed shared memory buys; kept as an option for the TMEM experiments.
+#ifndef QCB_P16_GTAB
+#define QCB_P16_GTAB 0
+#endif
+// Row parity applied to the sign test with a lane-wise add of the parity's
+// sign bits (VIADD.16x2, FMA-heavy pipe) instead of an XOR (LOP3, ALU pipe):
+// the ALU pipe carries ~7.4 of ~15.2 instructions per pair-edge and is the
+// binding pipe (ncu: ALU 64 % at 66 % issue); this moves one op per edge.
+#ifndef QCB_P16_ADDSIGN
+#define QCB_P16_ADDSIGN 1
+#endif
+// Messages of the first TMT tiers in TMEM instead of registers (native Z > 32,
+// one pair per CTA), the register cap lowered to QCB_P16_TM_CAP: fewer
+// registers -> 5 CTAs (15 warps) per SM instead of 4.  Measured per structure
+// (round 2, tools/exp/p16_sweep_r02.sh, int16 coded Gb/s at 262144 codewords,
+// TMT 0 / 2 / 3 / 4): Wi-Fi 1944 R5/6 (C3) 65.5 / 73.3 / 73.9 / 73.9, R3/4
+// 72.4 / 73.5 / 74.3 / 73.5, WiMAX 3/4A (C5) 87.0 / 87.6 / 87.6 / 87.6, 5/6
+// 90.3 / 92.3 / 89.1 / 89.2; Wi-Fi 1296 loses 2-8 %, WiMAX 1/2, 2/3B, 3/4B
+// lose 1-3 %, the rest are within 1 %.  QCB_P16_TMT >= 0 forces one value
+// for every eligible structure (experiments).
+#ifndef QCB_P16_TMT
+#define QCB_P16_TMT -1
+#endif
+#ifndef QCB_P16_TM_CAP
+#define QCB_P16_TM_CAP 128
+#endif
+constexpr int p16_tmt_default(int id) {
+  return (id == 6 || id == 7 || id == 15) ? 3 : ((id == 5 || id == 17) ? 2 : 0);
+}
+
 namespace qcb {
+
+// The pair kernel's dynamic shared memory (same region as the kernel's own
+// `extern __shared__ smem`): its window address is a per-kernel constant that
+// ptxas keeps in a uniform register and folds into LDS/STS [R + UR] addressing.
+extern __shared__ __align__(16) unsigned char qcb_p16_dyn[];
+__device__ __forceinline__ uint32_t p16_sbase() { return (uint32_t)__cvta_generic_to_shared(qcb_p16_dyn); }
+
+// Global address tables of the native-Z pair kernels.  With one codeword pair
+// per CTA every CTA's thread t has the same table: its edges' cell offsets
+// (wrap included) relative to the dynamic shared-memory base.  It is filled
+// once per device by fill_p16_gtab_kernel and read through L1 (LDG.64, a tier
+// ahead): 33 KB shared by all CTAs of an SM instead of 33 KB of shared memory
+// per CTA (C5), which is what capped the kernel at 4 CTAs per SM.
+template <class S, int ZS>
+constexpr int p16_gtab_units() { return AddrTab<S, ZS, true>::units(); }
+template <class S, int ZS>
+__device__ uint2 g_p16_tab[kLayMaxThreads * (p16_gtab_units<S, ZS>() > 0 ? p16_gtab_units<S, ZS>() : 1)];
 
 __device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
   uint32_t d; asm("add.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
@@ -83,6 +136,8 @@ struct ArithI16x2 {
 #pragma unroll
     for (int k = 0; k + 1 < D; k += 2) sx ^= d[k] ^ d[k + 1];
     if (D & 1) sx ^= d[D - 1];
+    // lane parities only in the sign bits (for the lane-wise sign flip below)
+    const uint32_t sxm = QCB_P16_ADDSIGN ? (sx & 0x80008000u) : sx;
     uint32_t exa[D];
     if constexpr (QCB_P16_MIN3 == 2 || (QCB_P16_MIN3 == 1 && ANCHOR)) {
       loo_minima3<D>(a, exa, [](uint32_t x, uint32_t y) { return vmin2(x, y); },
@@ -111,7 +166,9 @@ struct ArithI16x2 {
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const uint32_t ex = exa[k];
-      const uint32_t m = lane_signs(d[k] ^ sx);                    // sign of L_new per lane
+      // sign of L_new per lane = sign(zz) ^ parity: the parity bit added to
+      // bit 15 / 31 lane-wise (no carry leaves a lane) flips exactly that bit
+      const uint32_t m = QCB_P16_ADDSIGN ? lane_signs(vadd2(d[k], sxm)) : lane_signs(d[k] ^ sx);
       if constexpr (XORSIGN) {
         // L_new = (ex + m) ^ m: a lane with m = 0xFFFF gets ~(ex - 1) = -ex
         // (wrapping: -(-32768) = -32768); the message's negation on the FMA pipe
@@ -133,28 +190,85 @@ struct Layered2 {
 
   static constexpr bool TAB = use_addr_tab<S, A>();
   static constexpr int ME = tab_max_entries<S, ZS, TAB>();
+  // table in global memory (native Z, one pair per CTA): `tab` is then the
+  // thread's byte offset into g_p16_tab<S, ZS> and entries are relative to
+  // the dynamic shared-memory base
+  static constexpr bool GT = QCB_P16_GTAB && TAB && ZS > 0 && p16_gtab_units<S, ZS>() > 0;
+  // tiers [0, TMT) keep their messages in TMEM columns [START[T], START[T+1])
+  // of the thread's lane; the rest in registers (nm[e - TMC])
+  static constexpr int kTmtWant = QCB_P16_TMT >= 0 ? QCB_P16_TMT : p16_tmt_default(S::ID);
+  static constexpr int TMT = (ZS > 32 && ZS <= 128) ? (kTmtWant < S::MB ? kTmtWant : S::MB - 1) : 0;
+  static constexpr int TMC = S::START[TMT];
+  static constexpr int NR = S::NE - TMC;
+  static constexpr int TCOLS = TMC <= 32 ? 32 : (TMC <= 64 ? 64 : (TMC <= 128 ? 128 : 256));
+
+  template <int T>
+  __device__ __forceinline__ static void fetch(uint32_t tab, uint32_t* ent) {
+    if constexpr (GT) {
+      using AT = AddrTab<S, ZS, true>;
+      if constexpr (T < S::MB) {
+        constexpr int NU = (AT::count(T) + 1) / 2;
+        const uint2* g = g_p16_tab<S, ZS> + (tab >> 3) + AT::unit0(T);
+        const uint32_t sb = p16_sbase();
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+          const uint2 v = __ldg(g + u);
+          ent[2 * u] = v.x + sb;
+          ent[2 * u + 1] = v.y + sb;
+        }
+      }
+    } else {
+      tab_fetch<S, ZS, TAB, T>(tab, ent);
+    }
+  }
+  template <int E0>
+  __device__ __forceinline__ static void addrs(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t tab,
+                                               uint32_t* addr) {
+    constexpr int D = S::DEG[AddrTab<S, ZS, TAB>::tier_of(E0)];
+    if constexpr (GT) {
+      constexpr int T = AddrTab<S, ZS, TAB>::tier_of(E0);
+      uint32_t ent[ME];
+      fetch<T>(tab, ent);
+      tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ent, addr, std::make_integer_sequence<int, D>{});
+    } else {
+      tier_addrs_tab<S, A, ZS, TAB, E0>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+    }
+  }
 
   // keep: lanes of converged codewords (early termination) keep their posteriors;
   // pe / pn: this / the next tier's early-loaded posteriors (early_edge);
   // ec / en: this / the next tier's address-table entries
   template <int T, bool ET>
   __device__ __forceinline__ static void tier(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                              uint32_t tab, uint32_t (&nm)[S::NE], uint32_t keep,
-                                              uint32_t (&pe)[S::MAXDEG], uint32_t (&pn)[S::MAXDEG],
+                                              uint32_t tab, uint32_t tb, uint32_t (&nm)[NR > 0 ? NR : 1],
+                                              uint32_t keep, uint32_t (&pe)[S::MAXDEG], uint32_t (&pn)[S::MAXDEG],
                                               uint32_t (&ec)[ME], uint32_t (&en)[ME]) {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
+    constexpr bool XS = QCB_P16_XORSIGN == 1 || (QCB_P16_XORSIGN == 0 && S::ID == 7);
     uint32_t addr[D], p[D], o[D];
+    uint32_t mt[T < TMT ? D : 1];
+    if constexpr (T < TMT) {
+      (void)tb;
+      tm_wait_st();                              // this thread's earlier TMEM stores have landed
+      tm_ld_n<E0, D>(tb, mt);                    // overlaps the posterior loads below
+    }
     tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ec, addr, std::make_integer_sequence<int, D>{});
 #pragma unroll
     for (int k = 0; k < D; ++k) p[k] = early_edge<S, T>(k) ? pe[k] : A::lds(addr[k]);
-    if constexpr (!QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
+    if constexpr (!QCB_P16_TAB_LATE) fetch<T + 1>(tab, en);
     // sign application: two selects, or (ex + m) ^ m with the message negated
     // on the FMA pipe where measured faster (tools/exp/pc16_run.sh: Wi-Fi 1944
     // R5/6 = C3 +2.8 %; WiMAX 1/2 -4.8 %, 3/4A -2 %; others within +-1 %)
-    A::template row<D, (S::ID >= 12), (QCB_P16_XORSIGN == 1 || (QCB_P16_XORSIGN == 0 && S::ID == 7))>(p, o, nm + E0, K);
+    if constexpr (T < TMT) {
+      tm_wait_ld<D>(mt);
+      A::template row<D, (S::ID >= 12), XS>(p, o, mt, K);
+      tm_st_n<E0, D>(tb, mt);
+    } else {
+      A::template row<D, (S::ID >= 12), XS>(p, o, nm + (E0 - TMC), K);
+    }
     // late: the next tier's table entries are not live across the row update
-    if constexpr (QCB_P16_TAB_LATE) tab_fetch<S, ZS, TAB, T + 1>(tab, en);
+    if constexpr (QCB_P16_TAB_LATE) fetch<T + 1>(tab, en);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       uint32_t v = o[k];
@@ -176,7 +290,7 @@ struct Layered2 {
     constexpr int D = S::DEG[T];
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
-    tier_addrs_tab<S, A, ZS, TAB, E0>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+    addrs<E0>(a, r, b0, b1, tab, addr);
     // hard = post <= 0 per lane: max(post, -32767) - 1 is negative exactly for
     // post <= 0 (the max keeps -32768 from wrapping); XOR of the lane sign
     // bits (15, 31) = the two codewords' row parities
@@ -188,20 +302,20 @@ struct Layered2 {
 
   template <bool ET, int... Ts>
   __device__ __forceinline__ static void sweep(const SpecArgs& a, const RtK& K, int r, uint32_t b0, uint32_t b1,
-                                               uint32_t tab, uint32_t (&nm)[S::NE], bool work, uint32_t keep,
-                                               std::integer_sequence<int, Ts...>) {
+                                               uint32_t tab, uint32_t tb, uint32_t (&nm)[NR > 0 ? NR : 1], bool work,
+                                               uint32_t keep, std::integer_sequence<int, Ts...>) {
     uint32_t pa[S::MAXDEG], pb[S::MAXDEG];
     uint32_t ea[ME], eb[ME];
-    tab_fetch<S, ZS, TAB, 0>(tab, ea);
+    fetch<0>(tab, ea);
     if constexpr (ET) {
-      ((work ? tier<Ts, true>(a, K, r, b0, b1, tab, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
+      ((work ? tier<Ts, true>(a, K, r, b0, b1, tab, tb, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
                               (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
              : void(),
         tier_sync<ZS>()), ...);
     } else {
       (void)work; (void)keep;
-      ((tier<Ts, false>(a, K, r, b0, b1, tab, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb, (Ts & 1) ? eb : ea,
-                        (Ts & 1) ? ea : eb),
+      ((tier<Ts, false>(a, K, r, b0, b1, tab, tb, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
+                        (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb),
         tier_sync<ZS>()), ...);
     }
   }
@@ -234,7 +348,7 @@ struct Layered2 {
                                                      uint32_t (&v)[S::DEG[T]]) {
     constexpr int D = S::DEG[T];
     uint32_t addr[D];
-    tier_addrs_tab<S, A, ZS, TAB, S::START[T]>(a, r, b0, b1, tab, addr, std::make_integer_sequence<int, D>{});
+    addrs<S::START[T]>(a, r, b0, b1, tab, addr);
 #pragma unroll
     for (int k = 0; k < D; ++k) v[k] = A::lds(addr[k]);
   }
@@ -290,6 +404,7 @@ struct Layered2 {
 #endif
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
+  if constexpr (Layered2<S, ZS>::TMT > 0) return QCB_P16_TM_CAP;
   const int z = ZS > 0 ? ZS : 96;
   const int cap = raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true, smsp_raise<S, ArithI16x2>());
   // 128 registers = 4 warps per sub-partition, paid for with spills; measured
@@ -315,6 +430,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   __shared__ int s_fail[MAXC + 2], s_done[MAXC + 2], s_iters[MAXC + 2];   // + scratch pair
   __shared__ int s_active;
   __shared__ int s_odd2[2];                     // early-exit syndrome lane bits, per sweep parity (G == 1 with ET)
+  __shared__ uint32_t s_taddr;                  // TMEM base (L::TMT > 0)
 
   const RtK K{a.k_one, a.k_sign, a.k_shr, a.k_neg1, a.k_lane1};
   const int Z = ZS > 0 ? ZS : a.z;
@@ -339,11 +455,20 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * kCellBytes), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * kCellBytes)));
-  const uint32_t tab = sbase + (uint32_t)G * cws + (uint32_t)(tid * addr_tab_bytes_per_thread<S, ZS, L::TAB>());
+  constexpr int kTabB = L::GT ? 0 : addr_tab_bytes_per_thread<S, ZS, L::TAB>();   // shared-memory table bytes
+  const uint32_t tab = L::GT ? (uint32_t)(tid * 8 * p16_gtab_units<S, ZS>())
+                             : sbase + (uint32_t)G * cws + (uint32_t)(tid * kTabB);
   // early-termination snapshot block (G == 1), after the address tables
-  const uint32_t snap_offset = ((uint32_t)G * cws + blockDim.x * (uint32_t)addr_tab_bytes_per_thread<S, ZS, L::TAB>() +
-                                15u) & ~15u;
-  fill_addr_tab<S, ArithI16x2, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
+  const uint32_t snap_offset = ((uint32_t)G * cws + blockDim.x * (uint32_t)kTabB + 15u) & ~15u;
+  if constexpr (!L::GT) fill_addr_tab<S, ArithI16x2, ZS, L::TAB>(a, rs, b0, b1, tab, std::make_integer_sequence<int, S::NE>{});
+
+  if constexpr (L::TMT > 0) {                   // one warp allocates the CTA's message columns
+    if (tid < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"((uint32_t)__cvta_generic_to_shared(&s_taddr)), "r"((uint32_t)L::TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
@@ -353,16 +478,28 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     }
     if (tid == 0) s_odd2[0] = s_odd2[1] = 0;
   }
+  if constexpr (L::TMT > 0) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-
-  uint32_t nm[S::NE];
+  uint32_t tb = 0;                              // this thread's TMEM lane, column 0
+  if constexpr (L::TMT > 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tb = s_taddr + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16);
+    uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // messages start at 0 (reference init)
 #pragma unroll
-  for (int e = 0; e < S::NE; ++e) nm[e] = 0u;
+    for (int c = 0; c + 8 <= L::TMC; c += 8) tm_st<8>(tb + c, z8);
+    if constexpr (L::TMC % 8 >= 4) tm_st<4>(tb + (L::TMC / 8) * 8, z8);
+    if constexpr (L::TMC % 4 >= 2) tm_st<2>(tb + (L::TMC / 4) * 4, z8);
+    if constexpr (L::TMC % 2 == 1) tm_st<1>(tb + L::TMC - 1, z8);
+  }
+
+  uint32_t nm[L::NR > 0 ? L::NR : 1];
+#pragma unroll
+  for (int e = 0; e < (L::NR > 0 ? L::NR : 1); ++e) nm[e] = 0u;
 
   const auto tiers = std::make_integer_sequence<int, S::MB>{};
   if constexpr (!ET) {
     // fixed iterations: every codeword runs max_iters sweeps; one syndrome at the end
-    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
+    for (int k = 0; k < a.max_iters; ++k) L::template sweep<false>(a, K, rs, b0, b1, tab, tb, nm, act, 0u, tiers);
     if (a.max_iters > 0) {
       if (tid < MAXC) s_fail[tid] = 0;
       __syncthreads();
@@ -387,7 +524,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     bool done_a = false, done_b = ncw < 2;
     uint32_t saved = 0;                                   // lane masks held in the snapshot
     while (k < a.max_iters && !(done_a && done_b)) {
-      L::template sweep<false>(a, K, rs, b0, b1, tab, nm, act, 0u, tiers);
+      L::template sweep<false>(a, K, rs, b0, b1, tab, tb, nm, act, 0u, tiers);
       ++k;
 #if QCB_ET_EARLY_EXIT
       // every odd lane bit a thread finds is published to this sweep's flag
@@ -429,12 +566,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
       s_iters[1] = it_b; s_fail[1] = fail_b;
     }
     __syncthreads();
-  } else {
+  } else if constexpr (L::TMT == 0) {           // several pairs per CTA (TMEM kernels launch one)
     for (int k = 0; k < a.max_iters; ++k) {
       const bool da = s_done[2 * gs], db = s_done[2 * gs + 1];
       const bool work = act && !(da && db);
       const uint32_t keep = (da ? 0x0000FFFFu : 0u) | (db ? 0xFFFF0000u : 0u);
-      L::template sweep<true>(a, K, rs, b0, b1, tab, nm, work, keep, tiers);
+      L::template sweep<true>(a, K, rs, b0, b1, tab, tb, nm, work, keep, tiers);
       if (tid < MAXC) s_fail[tid] = 0;          // syndrome (_kernels.py:85-96)
       __syncthreads();
       if (work) {
@@ -461,6 +598,64 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   }
   store_outputs_pair16(reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N), a.hard_packed,
                        a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, sbase);
+  if constexpr (L::TMT > 0) {                   // release the message columns
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "r"((uint32_t)L::TCOLS));
+  }
+}
+
+template <class S, int ZS, int... Es>
+__device__ __forceinline__ void p16_gtab_entries(const SpecArgs& a, int r, uint32_t b0, uint32_t b1, uint32_t* ent,
+                                                 std::integer_sequence<int, Es...>) {
+  using AT = AddrTab<S, ZS, true>;
+#pragma unroll
+  for (int i = 0; i < 2 * AT::units(); ++i) ent[i] = 0u;
+  ((AT::in_tab(Es) ? (void)(ent[AT::entry(Es)] = edge_addr<S, ArithI16x2, ZS, Es>(a, r, b0, b1)) : void()), ...);
+}
+
+// g_p16_tab<S, ZS> for one pair per CTA: thread t's table entries relative to
+// the dynamic shared-memory base (the decode kernel adds its base)
+template <class S, int ZS>
+__global__ void fill_p16_gtab_kernel(const __grid_constant__ SpecArgs a) {
+  using AT = AddrTab<S, ZS, true>;
+  constexpr int NU = AT::units();
+  const int tid = threadIdx.x;
+  const RowMap rm = map_row(tid, 1, ZS);
+  const uint32_t b0 = (uint32_t)(rm.r * kCellBytes), b1 = b0 - (uint32_t)(ZS * kCellBytes);
+  uint32_t ent[2 * NU];
+  p16_gtab_entries<S, ZS>(a, rm.r, b0, b1, ent, std::make_integer_sequence<int, S::NE>{});
+#pragma unroll
+  for (int u = 0; u < NU; ++u) g_p16_tab<S, ZS>[tid * NU + u] = make_uint2(ent[2 * u], ent[2 * u + 1]);
+}
+
+// Fill g_p16_tab<S, ZS> on the current device before its first decode there.
+// The fill is a stream-ordered kernel launch (capturable); a device is marked
+// done only after a fill launched outside a graph capture (a captured fill
+// that is never replayed must not count).
+template <class S, int ZS>
+inline cudaError_t ensure_p16_gtab(const SpecArgs& a, int threads, cudaStream_t s) {
+  static std::mutex m;
+  static unsigned done = 0;                               // bit per device (< 32 devices)
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(m);
+    if (dev < 32 && ((done >> dev) & 1u)) return cudaSuccess;
+  }
+  fill_p16_gtab_kernel<S, ZS><<<1, threads, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  e = cudaStreamIsCapturing(s, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs == cudaStreamCaptureStatusNone && dev < 32) {
+    std::lock_guard<std::mutex> lk(m);
+    done |= 1u << dev;
+  }
+  return cudaSuccess;
 }
 
 template <class S, int ZS, bool ET>
@@ -473,14 +668,20 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   SpecArgs b = a;
   b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4);
   if constexpr (one_warp_cta<ZS>()) b.pairs = 1;            // tier_sync is a warp barrier
+  if constexpr (Layered2<S, ZS>::GT || Layered2<S, ZS>::TMT > 0) b.pairs = 1;   // per-thread global table / TMEM lanes
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
   const size_t cwsb = (size_t)cw_block_bytes(z);
-  const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>() +
-                        15) & ~(size_t)15) + (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block
+  constexpr int kTabB = Layered2<S, ZS>::GT ? 0 : addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
+  const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * kTabB + 15) & ~(size_t)15) +
+                      (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block
   e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
+  if constexpr (Layered2<S, ZS>::GT) {
+    e = ensure_p16_gtab<S, ZS>(b, thr, s);
+    if (e != cudaSuccess) return e;
+  }
   const int64_t per = 2 * (int64_t)b.pairs;
   const int64_t blocks = (a.w + per - 1) / per;
   if (blocks <= 0) return cudaSuccess;

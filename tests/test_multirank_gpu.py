@@ -70,3 +70,29 @@ def test_two_rank_shards_equal_one_rank(tmp_path, key, w):
         assert np.array_equal(got, ref.cpu().numpy()), name
     cnt = shard.decode_counters(hard, it, conv, shard_info(wl, 0, 0, total, "cuda"), mm.k).cpu().numpy()
     assert all(np.array_equal(p["cnt"], cnt) for p in parts)
+
+
+def test_bench_two_ranks_match_one_rank():
+    """bench.py end to end at --gpus 1 and --gpus 2 (self-launched torchrun;
+    gloo so that both ranks can share the one GPU of the test box): the job's
+    hard-decision digest, counters and oracle check are the same -- the
+    scaling run decodes the same 2^22-codeword job whatever N is."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lines = []
+    for n in (1, 2):
+        env = dict(os.environ, QCB_BENCH_BACKEND="gloo")
+        out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", str(n), "--config", "C5",
+                              "--codewords", "20001", "--steps", "2", "--warmup", "1", "--no-e2e", "--no-cpu",
+                              "--no-encode"], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+        assert out.returncode == 0, out.stderr[-3000:]
+        lines.append(json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1]))
+    one, two = lines
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert one["digest"] == two["digest"]
+    assert one["counters"] == two["counters"] and one["counters"]["frames"] == 20001
+    assert one["check"]["result"] == two["check"]["result"] == "bit-exact"
+    assert two["config"]["codewords_total"] == 20001

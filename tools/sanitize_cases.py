@@ -1,0 +1,130 @@
+"""Small launches of every libqcb200 kernel family, for compute-sanitizer.
+
+    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} \
+        python tools/sanitize_cases.py [--quick]
+
+One tool per run (B200_PROFILING.md: several tools in one call have left the
+GPU unusable).  Every case also checks its result against the CPU oracle, so
+a run that the sanitizer passes is also a parity run.  Sizes are tiny (a few
+codewords / tiles): racecheck instruments every shared-memory access.
+
+Cases (the hazards named in VERDICT r1 "What's missing" 4):
+  * float32 register kernel, native Z (WiMAX 2304 R1/2 = C2's kernel; Wi-Fi 648
+    R1/2 = C1's one-warp CTA with __syncwarp tiers and shadow lanes (Z = 27)),
+    early termination on / off (the s_odd syndrome flags, polled through a
+    volatile shared word);
+  * int16 pair kernel (C5's WiMAX 2304 R3/4A with the global address table;
+    Wi-Fi 1944 R5/6 = C3, Z = 81 with shadow lanes), ET on / off, an odd
+    number of codewords (a half-empty pair);
+  * runtime-Z kernels on a scaled code, the TMEM float32 kernel, the generic
+    kernel;
+  * misaligned (element-offset) LLR / output views: scalar prologue/epilogue;
+  * encoders: TMA bulk-copy Z=96 pipeline (full tiles + ragged tail), the
+    bit-granular Wi-Fi pipeline (atomicOr on boundary words), staged and
+    generic encoders, encode_array;
+  * channel: frames_info, channel_llr (f32 / int16), count_errors, records.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+    import paper_2306_12063_b200 as P
+    from oracle import oracle as O
+    from paper_2306_12063_b200 import channel as CH, llrio
+    from tests._util import noisy_llrs
+
+    torch.cuda.set_device(0)
+    rng = np.random.default_rng(11)
+    quick = "--quick" in sys.argv
+    n_ok = 0
+
+    def dec(mm, w, fixed, early, iters=3, misalign=False, tag=""):
+        nonlocal n_ok
+        llr, _, _ = noisy_llrs(mm, w, 2.5, seed=int(rng.integers(1 << 30)), fixed=fixed)
+        cfg = P.DecoderConfig(max_iterations=iters, early_termination=early,
+                              arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
+        t = torch.from_numpy(llr).cuda()
+        if misalign:
+            flat = torch.empty(llr.size + 1, dtype=t.dtype, device="cuda")
+            flat[1:] = t.reshape(-1)
+            t = flat[1:].view(llr.shape)
+        hard, it, conv, post = P.decode_batch(mm, t, cfg, posteriors=True)
+        hp, _, _ = P.decode_batch(mm, t, cfg, hard_packed=True)
+        torch.cuda.synchronize()
+        oh, oi, oc = O.decode_batch(P.expand(mm), llr, iters, early)
+        assert np.array_equal(hard.cpu().numpy(), oh), tag
+        assert np.array_equal(it.cpu().numpy(), oi) and np.array_equal(conv.cpu().numpy(), oc), tag
+        assert np.array_equal(hp.cpu().numpy(), np.packbits(oh, axis=-1)), tag
+        n_ok += 1
+        print("ok", tag, flush=True)
+
+    cases = [
+        (("wimax", 2304, "1/2"), False), (("wifi", 648, "1/2"), False),
+        (("wimax", 2304, "3/4A"), True), (("wifi", 1944, "5/6"), True),
+        (("wimax", 960, "3/4A"), False), (("wimax", 960, "3/4A"), True),      # runtime Z (scaled)
+        (("wifi", 1296, "2/3"), True),                                         # Z = 54, global table
+    ]
+    for code, fixed in cases:
+        mm = P.get_model_matrix(*code)
+        for early in ((False, True) if not quick else (False,)):
+            dec(mm, 3, fixed, early, tag=f"{code} fixed={fixed} et={early}")
+    dec(P.get_model_matrix("wimax", 2304, "3/4A"), 5, True, False, misalign=True, tag="misaligned int16")
+    dec(P.get_model_matrix("wimax", 2304, "1/2"), 3, False, True, misalign=True, tag="misaligned f32")
+    # TMEM float32 kernel (the default for scaled degree-20 codes with Z >= 40)
+    dec(P.get_model_matrix("wimax", 1152, "5/6"), 3, False, True, tag="tmem f32")
+    # generic kernel
+    ent = rng.integers(-1, 17, size=(4, 10))
+    ent[:, 0] = rng.integers(0, 17, size=4)
+    gen = P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 17, 10, 6, ent)
+    for fixed in (False, True):
+        dec(gen, 3, fixed, True, tag=f"generic fixed={fixed}")
+
+    # encoders
+    for code, w in ((("wimax", 2304, "3/4A"), 300), (("wimax", 2304, "1/2"), 129), (("wimax", 576, "2/3B"), 77)):
+        mm = P.get_model_matrix(*code)
+        info = rng.integers(0, 256, size=(w, mm.k // 8), dtype=np.uint8)
+        got = P.encode_packed(P.make_plan(mm, P.EncoderVariant.Packed), torch.from_numpy(info).cuda())
+        assert np.array_equal(got.cpu().numpy(), O.encode_packed(mm, info)), code
+        n_ok += 1
+        print("ok encode_packed", code, w, flush=True)
+    for code, w in ((("wifi", 1944, "1/2"), 300), (("wifi", 648, "5/6"), 131), (("wimax", 672, "3/4A"), 50)):
+        mm = P.get_model_matrix(*code)
+        bits = rng.integers(0, 2, size=(w, mm.k), dtype=np.uint8)
+        got = P.encode_bits(mm, torch.from_numpy(P.pack_bits(bits)).cuda()).cpu().numpy()
+        assert np.array_equal(got, P.pack_bits(P.encode_array(P.make_plan(mm), bits))), code
+        n_ok += 1
+        print("ok encode_bits", code, w, flush=True)
+
+    # channel + counters + records
+    mm = P.get_model_matrix("wimax", 576, "1/2")
+    info = CH.frames_info_device(3, 0, 10, 40, mm.k, "cuda")
+    cw = CH.encode_array_device(mm, info)
+    assert np.array_equal(cw.cpu().numpy(), P.encode_array(P.make_plan(mm), info.cpu().numpy()))
+    for arith in (P.Arithmetic.Float32, P.Arithmetic.Fixed16):
+        llr = CH.channel_llr_device(cw, 0.5, arith, seed=3, frame0=10)
+        hard, it, conv = P.decode_batch(mm, llr, P.DecoderConfig(arithmetic=arith, max_iterations=4))
+        sums = CH.count_errors_device(hard, info, it, mm.k, batch=16)
+        hp, _, _ = P.decode_batch(mm, llr, P.DecoderConfig(arithmetic=arith, max_iterations=4), hard_packed=True)
+        rec = llrio.pack_records_device(hp, it, conv, mm.n)
+        torch.cuda.synchronize()
+        assert int(sums[:, 2].sum()) == int(it.sum()) and rec.shape == (40, mm.n // 8 + 2)
+        n_ok += 1
+        print("ok channel", arith.value, flush=True)
+    q = CH.quantize_llr_device(torch.randn(1000, device="cuda") * 30)
+    torch.cuda.synchronize()
+    assert int(q.abs().max()) <= 1023
+    print(f"sanitize cases: {n_ok + 1} groups ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
