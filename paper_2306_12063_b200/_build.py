@@ -39,7 +39,10 @@ def nvcc() -> str:
 
 
 def _sources():
-    return sorted(CSRC.glob("*.cu"))
+    src = sorted(CSRC.glob("*.cu"))
+    if "-DQCB_SCALED_KERNELS=0" in EXTRA:          # experiment builds: no per-Z scaled decoders
+        src = [s for s in src if not s.name.startswith("dec_scaled_")]
+    return src
 
 
 def _deps():

@@ -166,9 +166,10 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
     a.llr = llr; a.hard = hard; a.iters = iters; a.conv = conv; a.post = post;
     a.w = w; a.n = c->n; a.z = c->z; a.max_iters = max_iters; a.early_term = early_term ? 1 : 0;
     a.hard_packed = hard_packed ? 1 : 0;
-    spec_plan(c->structure, elem, c->z, c->native ? 1 : 0, w, &a.pairs, &a.tmem_cols, &a.pair16);
-    const int cell = a.pair16 ? 4 : elem;                  // int16 pairs share one 4-byte cell
     a.native = c->native ? 1 : 0;
+    a.scaled = (!c->native && c->scaled) ? 1 : 0;
+    spec_plan(c->structure, elem, c->z, (a.native || a.scaled) ? 1 : 0, w, &a.pairs, &a.tmem_cols, &a.pair16);
+    const int cell = a.pair16 ? 4 : elem;                  // int16 pairs share one 4-byte cell
     a.k_one = 1u; a.k_sign = 0x80000000u; a.k_shr = 0x80000001u; a.k_neg1 = 0xFFFFFFFFu; a.k_lane1 = 0x00010001u;
     for (int i = 0; i < c->ne; ++i) {
       a.off[i] = (c->ent_j[i] * c->z + c->ent_e[i]) * cell;   // cell (c = r + e, j) at 4 (j Z + c)

@@ -5,6 +5,7 @@
 // :147-170 int16 with two's-complement wrap after every op).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "structures_gen.cuh"
@@ -22,6 +23,18 @@ constexpr int kMaxGenericTiers = 256;
 constexpr int kCellBytes = 4;
 constexpr int kStdNb = 24;
 __host__ __device__ constexpr int cw_block_bytes(int z) { return kStdNb * z * kCellBytes; }   // multiple of 16
+
+// Circulant shift of structure entry e at lifting size Z: the structure's own
+// table at Z0, else the 802.16e scaling of the Z0 = 96 WiMAX table
+// (reference codebook.py:217-229 / scale_model_matrix: p mod Z for rate 2/3A,
+// floor(p Z / 96) otherwise; p <= 0 unchanged).  Used by the encoders and by
+// the decoders compiled for a scaled WiMAX code's Z.
+template <class S, int Z>
+constexpr int zshift(int e) {
+  const int p = S::SHIFT0[e];
+  if (Z == S::Z0 || p <= 0) return p;
+  return std::is_same<S, S_wimax_r23a>::value ? p % Z : p * Z / 96;
+}
 
 // ---- exact float32 helpers -------------------------------------------------
 __device__ __forceinline__ float f_inf() { return __int_as_float(0x7f800000); }

@@ -47,6 +47,7 @@
 #include "decode_io.cuh"
 #include "kernels.h"
 #include "launch_cache.h"
+#include "scaled_plan_gen.h"
 
 // early-termination syndrome with early exit (measured: tools/exp/ab_et.sh)
 #ifndef QCB_ET_EARLY_EXIT
@@ -329,7 +330,7 @@ struct ArithF32 {
 template <class S, class A, int ZS, int E>
 __device__ __forceinline__ uint32_t edge_addr(const SpecArgs& a, int r, uint32_t b0, uint32_t b1) {
   if constexpr (ZS > 0) {
-    constexpr int sh = S::SHIFT0[E];
+    constexpr int sh = zshift<S, ZS>(E);
     constexpr uint32_t off = (uint32_t)((S::COL[E] * ZS + sh) * A::kElem);   // cell (c = r + sh, j)
     if constexpr (sh == 0) return b0 + off;
     else return (r >= ZS - sh ? b1 : b0) + off;
@@ -374,14 +375,16 @@ constexpr bool use_addr_tab() {
   // re-measured after the 3-input minima and register caps (tools/exp/tab_ab.sh):
   // Wi-Fi 648 R1/2 drops its table (+2.7 %), 648 R3/4 and 1296 R2/3 take one
   // (+6.9 / +1.8 %); float32 unchanged (all / none within 1 % of this policy)
-  constexpr unsigned kPair16 = 0x7u | (0x7u << 4) | (0x3u << 9) | (0x3Fu << 12);
+  // round 2: Wi-Fi 1944 R5/6 (C3) takes one too now that its first tiers'
+  // messages sit in TMEM: 89.7 -> 97.8 Gb/s (tools/exp/r02_call4.sh)
+  constexpr unsigned kPair16 = 0x7u | (0xFu << 4) | (0x3u << 9) | (0x3Fu << 12);
 #endif
   return QCB_ADDR_TAB && ((A::kKind == 0 && ((kF32 >> S::ID) & 1u)) || (A::kKind == 2 && ((kPair16 >> S::ID) & 1u)));
 }
 
 template <class S, int ZS, bool TAB>
 struct AddrTab {
-  static constexpr bool in_tab(int e) { return TAB && (ZS == 0 || S::SHIFT0[e] != 0); }
+  static constexpr bool in_tab(int e) { return TAB && (ZS == 0 || zshift<S, ZS>(e) != 0); }
   static constexpr int tier_of(int e) {
     int t = 0;
     while (S::START[t + 1] <= e) ++t;
@@ -564,11 +567,21 @@ __device__ __forceinline__ void sts128f(uint32_t a, float x, float y, float z, f
 #ifndef QCB_WARP_SYNC
 #define QCB_WARP_SYNC 1
 #endif
-template <int ZS>
-constexpr bool one_warp_cta() { return QCB_WARP_SYNC && ZS > 0 && ZS <= 32; }
-template <int ZS>
+#ifndef QCB_Z24_CTA
+#define QCB_Z24_CTA 0      // 1: Z = 24 codes take CTA barriers (several codewords per CTA) instead
+#endif
+// KIND = the arithmetic's kKind.  The int16 pair kernel at Z = 24 (scaled
+// WiMAX N = 576) instead packs four codeword pairs into three full warps with
+// CTA barriers: 90.7 vs 78.7 Gb/s (WiMAX 576 R1/2; +10..21 % on all six
+// rates), where float32 keeps the one-warp CTA (72.2 vs 61.8 at G = 1, 60.6
+// at G = 4; round 2, tools/exp/r02_call4.sh).
+template <int ZS, int KIND = 0>
+constexpr bool one_warp_cta() {
+  return QCB_WARP_SYNC && ZS > 0 && ZS <= 32 && !((QCB_Z24_CTA || KIND == 2) && ZS == 24);
+}
+template <int ZS, int KIND = 0>
 __device__ __forceinline__ void tier_sync() {
-  if constexpr (one_warp_cta<ZS>()) __syncwarp();
+  if constexpr (one_warp_cta<ZS, KIND>()) __syncwarp();
   else __syncthreads();
 }
 
@@ -841,6 +854,9 @@ constexpr int reg_cap() {
 #else
   constexpr int kMax = ((((1u << 6) | (1u << 13) | (1u << 15)) >> S::ID) & 1u) ? 128 : 255;
 #endif
+#ifdef QCB_F32_SCALED_CAP                              // tuning experiments: scaled Z only
+  if constexpr (ZS > 0 && ZS != S::Z0) return cap > QCB_F32_SCALED_CAP ? QCB_F32_SCALED_CAP : cap;
+#endif
   return cap > kMax ? kMax : cap;
 }
 
@@ -965,12 +981,30 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 }
 
 // codewords per CTA for a kernel with `regs` registers per thread
-inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes) {
+// Codewords (int16 kernel: codeword pairs) per CTA where Z leaves lanes of the
+// last warp idle (the scaled WiMAX codes): G codewords' rows are dealt out
+// contiguously over ceil(G Z / 32) warps, so a G with G Z near a multiple of
+// 32 busies more lanes, at the price of a tier barrier over more warps.
+// Measured per scaled code for G = 1..4 (scaled_plan_gen.h): Z = 36, 40 take
+// G = 3 (+25-39 %), Z = 44, 48 G = 2 (+15-23 %), Z = 68-84 G = 3 on the
+// lower-degree structures; full or nearly full Z keep G = 1.
+inline const ScaledPlan* scaled_plan(int structure_id, int elem, int z) {
+  for (int i = 0; i < kScaledPlans; ++i)
+    if (kScaledPlan[i].id == structure_id && kScaledPlan[i].elem == elem && kScaledPlan[i].z == z) return &kScaledPlan[i];
+  return nullptr;
+}
+inline int lane_fill_cw(int z, int kind, int structure_id) {
+  const ScaledPlan* p = scaled_plan(structure_id, kind == 2 ? 2 : 4, z);
+  return p ? p->g : 1;
+}
+
+inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes, int fill = 1) {
   static const int env_v = [] {                        // tuning knob (benchmarks only)
     const char* env = getenv("QCB_CW_PER_CTA");
     return env ? atoi(env) : 0;
   }();
   if (env_v >= 1 && env_v <= kLayMaxCw && env_v * z <= kLayMaxThreads) return env_v;
+  if (fill > 1 && fill * z <= kLayMaxThreads && w >= (int64_t)fill * 148 * 4) return fill;
   const int sms = device_sm_count();
   (void)cell_bytes;
   const int cw_smem = cw_block_bytes(z);
@@ -1001,7 +1035,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   cudaError_t e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
-  b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem);
+  b.pairs = layered_cw_per_cta(z, a.w, fa.numRegs, A::kElem, ZS == S::Z0 ? 1 : lane_fill_cw(z, A::kKind, S::ID));
   if constexpr (one_warp_cta<ZS>()) b.pairs = 1;            // tier_sync is a warp barrier
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;

@@ -197,7 +197,8 @@ struct Layered2 {
   // tiers [0, TMT) keep their messages in TMEM columns [START[T], START[T+1])
   // of the thread's lane; the rest in registers (nm[e - TMC])
   static constexpr int kTmtWant = QCB_P16_TMT >= 0 ? QCB_P16_TMT : p16_tmt_default(S::ID);
-  static constexpr int TMT = (ZS > 32 && ZS <= 128) ? (kTmtWant < S::MB ? kTmtWant : S::MB - 1) : 0;
+  // (measured on the native codes only: scaled Z keep every message in registers)
+  static constexpr int TMT = (ZS == S::Z0 && ZS > 32 && ZS <= 128) ? (kTmtWant < S::MB ? kTmtWant : S::MB - 1) : 0;
   static constexpr int TMC = S::START[TMT];
   static constexpr int NR = S::NE - TMC;
   static constexpr int TCOLS = TMC <= 32 ? 32 : (TMC <= 64 ? 64 : (TMC <= 128 ? 128 : 256));
@@ -311,12 +312,12 @@ struct Layered2 {
       ((work ? tier<Ts, true>(a, K, r, b0, b1, tab, tb, nm, keep, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
                               (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb)
              : void(),
-        tier_sync<ZS>()), ...);
+        tier_sync<ZS, 2>()), ...);
     } else {
       (void)work; (void)keep;
       ((tier<Ts, false>(a, K, r, b0, b1, tab, tb, nm, 0u, (Ts & 1) ? pb : pa, (Ts & 1) ? pa : pb,
                         (Ts & 1) ? eb : ea, (Ts & 1) ? ea : eb),
-        tier_sync<ZS>()), ...);
+        tier_sync<ZS, 2>()), ...);
     }
   }
 
@@ -416,6 +417,9 @@ constexpr int p16_reg_cap() {
 #else
   constexpr int kMax =
       ((((1u << 0) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 13) | (1u << 14)) >> S::ID) & 1u) ? 128 : 255;
+#endif
+#ifdef QCB_P16_SCALED_CAP                              // tuning experiments: scaled Z only
+  if constexpr (ZS > 0 && ZS != S::Z0) return cap > QCB_P16_SCALED_CAP ? QCB_P16_SCALED_CAP : cap;
 #endif
   return cap > kMax ? kMax : cap;
 }
@@ -666,8 +670,8 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   cudaError_t e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
-  b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4);
-  if constexpr (one_warp_cta<ZS>()) b.pairs = 1;            // tier_sync is a warp barrier
+  b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4, ZS == S::Z0 ? 1 : lane_fill_cw(z, 2, S::ID));
+  if constexpr (one_warp_cta<ZS, 2>()) b.pairs = 1;         // tier_sync is a warp barrier
   if constexpr (Layered2<S, ZS>::GT || Layered2<S, ZS>::TMT > 0) b.pairs = 1;   // per-thread global table / TMEM lanes
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;

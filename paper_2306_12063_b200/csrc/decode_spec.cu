@@ -1,7 +1,8 @@
 // decode_spec.cu -- host-side dispatch to the specialised layered decoders.
 // The kernel template lives in decode_layered.cuh; its 18 structures x
 // {float32, int16} x {native Z, runtime Z} x {early termination on, off}
-// instantiations are split over spec_part{0..5}.cu so they compile in parallel.
+// instantiations are split over spec_part{0..5}.cu so they compile in parallel;
+// the scaled WiMAX codes' per-Z instantiations are in dec_scaled_*.cu.
 #include "decode_pair16.cuh"
 #include "decode_tmem.cuh"
 
@@ -14,7 +15,46 @@ cudaError_t launch_spec_part3(int, int, const SpecArgs&, cudaStream_t);
 cudaError_t launch_spec_part4(int, int, const SpecArgs&, cudaStream_t);
 cudaError_t launch_spec_part5(int, int, const SpecArgs&, cudaStream_t);
 
+#ifndef QCB_SCALED_KERNELS
+#define QCB_SCALED_KERNELS 1      // 0: scaled codes take the runtime-Z kernels (experiment builds skip dec_scaled_*.cu)
+#endif
+
+#if QCB_SCALED_KERNELS
+#define QCB_SCALED_DECL(R) \
+  cudaError_t launch_scaled_##R##_lo(int, int, const SpecArgs&, cudaStream_t); \
+  cudaError_t launch_scaled_##R##_hi(int, int, const SpecArgs&, cudaStream_t);
+QCB_SCALED_DECL(r12) QCB_SCALED_DECL(r23a) QCB_SCALED_DECL(r23b)
+QCB_SCALED_DECL(r34a) QCB_SCALED_DECL(r34b) QCB_SCALED_DECL(r56)
+#undef QCB_SCALED_DECL
+
+// scaled WiMAX codes: the kernels compiled for their Z (decode_scaled.cuh)
+cudaError_t launch_scaled(int structure_id, int elem, const SpecArgs& a, cudaStream_t s) {
+  const int z = a.z;
+  const bool lo = z <= 56;
+#define QCB_SCALED_CASE(R, S) \
+  if (structure_id == S::ID) return lo ? launch_scaled_##R##_lo(z, elem, a, s) : launch_scaled_##R##_hi(z, elem, a, s);
+  QCB_SCALED_CASE(r12, S_wimax_r12)
+  QCB_SCALED_CASE(r23a, S_wimax_r23a)
+  QCB_SCALED_CASE(r23b, S_wimax_r23b)
+  QCB_SCALED_CASE(r34a, S_wimax_r34a)
+  QCB_SCALED_CASE(r34b, S_wimax_r34b)
+  QCB_SCALED_CASE(r56, S_wimax_r56)
+#undef QCB_SCALED_CASE
+  return cudaErrorInvalidValue;
+}
+#else
+cudaError_t launch_scaled(int, int, const SpecArgs&, cudaStream_t) { return cudaErrorInvalidValue; }
+#endif
+
 cudaError_t launch_spec(int structure_id, int elem, const SpecArgs& a, cudaStream_t s) {
+  static const bool scaled_env = [] {
+    const char* e = getenv("QCB_SCALED");
+    return !(e && e[0] == '0');
+  }();
+  if (QCB_SCALED_KERNELS && scaled_env && a.scaled && !a.native) {
+    const cudaError_t e = launch_scaled(structure_id, elem, a, s);
+    if (e != cudaErrorInvalidValue) return e;
+  }
   switch (structure_id % 6) {
     case 0: return launch_spec_part0(structure_id, elem, a, s);
     case 1: return launch_spec_part1(structure_id, elem, a, s);
@@ -102,7 +142,11 @@ void spec_plan(int structure_id, int elem, int z, int native, int64_t w, int32_t
 #ifndef QCB_TMEM_SCALED
 #define QCB_TMEM_SCALED 1
 #endif
-  const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20 && QCB_TMEM_SCALED && !native && z >= 40;
+  // compile-time kernels (native or scaled Z): TMEM where the per-code sweep
+  // measured it ahead (scaled_plan_gen.h: WiMAX R5/6 at Z = 68..76)
+  const ScaledPlan* sp = native ? scaled_plan(structure_id, elem, z) : nullptr;
+  const bool prefer = elem == 4 && maxdeg >= 18 && maxdeg <= 20 && QCB_TMEM_SCALED &&
+                      (native ? (sp && sp->tmem) : z >= 40);
   if (tmem_env == 1 || prefer) {
     *cw_per_cta = g;
     *tmem_cols = cols;

@@ -25,15 +25,6 @@ constexpr int entry_at(int t, int j) {   // entry index of block (t, j); -1 = ze
   return -1;
 }
 
-// shift of entry e at Z: the structure's own table at Z0, else the 802.16e
-// scaling of the Z0 = 96 WiMAX table (codebook.py:217-229 / scale_model_matrix:
-// p mod Z for rate 2/3A, floor(p Z / 96) otherwise; p <= 0 unchanged)
-template <class S, int Z>
-constexpr int zshift(int e) {
-  const int p = S::SHIFT0[e];
-  if (Z == S::Z0 || p <= 0) return p;
-  return std::is_same<S, S_wimax_r23a>::value ? p % Z : p * Z / 96;
-}
 
 template <class S, int Z = S::Z0>
 constexpr int hb_y_shift() {             // the single interior h_b entry (find_y, encoder.py:39-46)

@@ -38,6 +38,8 @@ struct SpecArgs {
   int32_t pairs;   // codewords per CTA
   int32_t tmem_cols;  // TMEM columns per CTA (TMEM-resident message kernel), 0 = register kernel
   int32_t native;     // 1: z == S::Z0 and shifts == S::SHIFT0 (compile-time shift kernel)
+  int32_t scaled;     // 1: WiMAX structure at z in 24..92 with the 802.16e-scaled shifts
+                      //    (compile-time kernel for that z, decode_scaled.cuh)
   uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
   uint32_t k_lane1;   // 0x00010001 (16x2 lane constant)
   int32_t pair16;     // int16 only: 1 = two codewords per thread in 16x2 lanes (pairs = codeword pairs per CTA)

@@ -547,3 +547,43 @@ print("ok")
     env = dict(os.environ, QCB_TMEM="1")
     res = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout + res.stderr
+
+
+SCALED_Z = list(range(24, 93, 4))
+
+
+@pytest.mark.parametrize("fixed", [False, True])
+def test_scaled_codes_compile_time_kernels_at_plan_size_match_oracle(fixed):
+    """The 108 scaled WiMAX codes run decoders compiled for their own Z
+    (csrc/decode_scaled.cuh) with the measured codewords-per-CTA plan
+    (csrc/scaled_plan_gen.h), which only engages for batches of several waves:
+    10,000 codewords per code here, device channel frames, every code, fixed
+    iterations (and early termination on a Z subset), checked against the C
+    oracle on sampled rows: the first and last CTAs' codewords (including a
+    ragged final CTA) and random rows in between."""
+    from paper_2306_12063_b200 import channel as CH
+    from tests._util import sigma2
+    dev = torch.device("cuda", 0)
+    arith = P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32
+    rng = np.random.default_rng(77 + fixed)
+    w = 10_001
+    for ci, (std, n, rate) in enumerate(P.supported_codes()):
+        if std != "wimax" or n == 2304:
+            continue
+        mm = P.get_model_matrix(std, n, rate)
+        h = P.expand(mm)
+        info = CH.frames_info_device(31, ci, 0, w, mm.k, dev)
+        llr = CH.channel_llr_device(CH.encode_array_device(mm, info), sigma2(1.5 + 2 * mm.rate.fraction,
+                                                                             mm.rate.fraction), arith, seed=31, point=ci)
+        rows = np.unique(np.concatenate([np.arange(40), np.arange(w - 40, w), rng.integers(0, w, 40)]))
+        llr_rows = llr[torch.from_numpy(rows).to(dev)].cpu().numpy()
+        for early in ((False, True) if mm.z in (24, 36, 48, 72, 84) else (False,)):
+            cfg = P.DecoderConfig(max_iterations=5, arithmetic=arith, early_termination=early)
+            hard, it, conv, post = P.decode_batch(mm, llr, cfg, posteriors=True)
+            torch.cuda.synchronize()
+            oh, oi, oc, op = O.decode_batch(h, llr_rows, 5, early, workers=4, want_post=True)
+            sel = torch.from_numpy(rows).to(dev)
+            assert np.array_equal(hard[sel].cpu().numpy(), oh), (n, rate, early)
+            assert np.array_equal(it[sel].cpu().numpy(), oi) and np.array_equal(conv[sel].cpu().numpy(), oc), (n, rate)
+            assert _post_equal(post[sel].cpu().numpy(), op), (n, rate, early)
+        del llr, info
