@@ -168,6 +168,10 @@ int decode_device(qc_code_t c, const T* llr, int64_t w, int32_t max_iters, int32
     a.hard_packed = hard_packed ? 1 : 0;
     a.native = c->native ? 1 : 0;
     a.scaled = (!c->native && c->scaled) ? 1 : 0;
+#if QCB_DEBUG_CHECKS
+    static const int inject = getenv("QCB_DEBUG_INJECT") ? 1 : 0;   // negative control of debug_checks.cuh
+    a.dbg_inject = inject;
+#endif
     spec_plan(c->structure, elem, c->z, (a.native || a.scaled) ? 1 : 0, w, &a.pairs, &a.tmem_cols, &a.pair16);
     const int cell = a.pair16 ? 4 : elem;                  // int16 pairs share one 4-byte cell
     a.k_one = 1u; a.k_sign = 0x80000000u; a.k_shr = 0x80000001u; a.k_neg1 = 0xFFFFFFFFu; a.k_lane1 = 0x00010001u;

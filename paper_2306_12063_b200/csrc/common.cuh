@@ -8,6 +8,7 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include "debug_checks.cuh"
 #include "structures_gen.cuh"
 
 namespace qcb {

@@ -32,19 +32,23 @@ template <int ZS>
 constexpr bool io_cells8() { return ZS > 0 && ZS % 32 != 0; }
 
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  dbg_smem(a, 4, 1);
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
+  dbg_smem(a, 4, 2);
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  dbg_smem(a, 16, 3);
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
+  dbg_smem(a, 16, 4);
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }

@@ -221,8 +221,14 @@ struct ArithF32 {
   static constexpr int kElem = 4;        // bytes per shared-memory cell
   static constexpr int kKind = 0;        // address-table policy key (use_addr_tab)
 
-  __device__ static Val lds(uint32_t a) { float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v; }
-  __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+  __device__ static Val lds(uint32_t a) {
+    dbg_smem(a, 4, 9);
+    float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a)); return v;
+  }
+  __device__ static void sts(uint32_t a, Val v) {
+    dbg_smem(a, 4, 10);
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+  }
   __device__ static bool hard(Val v) { return v <= 0.0f; }
   __device__ static Val zero() { return 0.0f; }   // reference init: min1 = min2 = 0, no signs -> L = +0.0
   // Channel LLRs enter shared memory as v + 0.0f: -0.0 becomes +0.0 and any
@@ -414,10 +420,12 @@ struct AddrTab {
 
 __device__ __forceinline__ uint2 lds64(uint32_t a) {
   uint2 v;
+  dbg_smem(a, 8, 5);
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  dbg_smem(a, 8, 6);
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
 }
 
@@ -554,12 +562,54 @@ struct SmemMsg {
 
 __device__ __forceinline__ float4 lds128f(uint32_t a) {
   float4 v;
+  dbg_smem(a, 16, 7);
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void sts128f(uint32_t a, float x, float y, float z, float w) {
+  dbg_smem(a, 16, 8);
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
+
+// The layered schedule runs the Z rows of a tier concurrently (one thread
+// per row, one barrier per tier).  That equals the reference's sequential row
+// loop (_kernels.py:47-48) only if no two rows of a tier touch the same
+// posterior cell: each circulant is a permutation of the Z cells of its block
+// column, so it suffices that a tier holds every block column at most once
+// (codebook.py:249).  Checked here at compile time for every
+// structure, together with the shift ranges at the native Z0 and at every
+// scaled Z the per-Z decoders are compiled for.
+template <class S>
+constexpr bool tiers_column_disjoint() {
+  for (int t = 0; t < S::MB; ++t)
+    for (int e = S::START[t]; e < S::START[t + 1]; ++e)
+      for (int f = e + 1; f < S::START[t + 1]; ++f)
+        if (S::COL[e] == S::COL[f]) return false;
+  return true;
+}
+template <class S, int Z>
+constexpr bool shifts_in_range() {
+  for (int e = 0; e < S::NE; ++e)
+    if (zshift<S, Z>(e) < 0 || zshift<S, Z>(e) >= Z) return false;
+  return true;
+}
+template <class S>
+constexpr bool scaled_shifts_in_range() {
+  if constexpr (S::Z0 != 96) return true;
+  else
+    return shifts_in_range<S, 24>() && shifts_in_range<S, 28>() && shifts_in_range<S, 32>() &&
+           shifts_in_range<S, 36>() && shifts_in_range<S, 40>() && shifts_in_range<S, 44>() &&
+           shifts_in_range<S, 48>() && shifts_in_range<S, 52>() && shifts_in_range<S, 56>() &&
+           shifts_in_range<S, 60>() && shifts_in_range<S, 64>() && shifts_in_range<S, 68>() &&
+           shifts_in_range<S, 72>() && shifts_in_range<S, 76>() && shifts_in_range<S, 80>() &&
+           shifts_in_range<S, 84>() && shifts_in_range<S, 88>() && shifts_in_range<S, 92>();
+}
+#define QCB_STRUCT_CHECKS(STRUCT)                                                            \
+  static_assert(tiers_column_disjoint<STRUCT>(), "a tier holds a block column twice");     \
+  static_assert(shifts_in_range<STRUCT, STRUCT::Z0>(), "native shift outside [0, Z0)");    \
+  static_assert(scaled_shifts_in_range<STRUCT>(), "scaled shift outside [0, Z)");
+QCB_FOR_EACH_STRUCTURE(QCB_STRUCT_CHECKS)
+#undef QCB_STRUCT_CHECKS
 
 // Tier barrier.  A one-warp CTA (native Z <= 32: Wi-Fi 648, one codeword per
 // CTA, forced at launch) needs no CTA barrier between tiers: __syncwarp
@@ -857,6 +907,10 @@ constexpr int reg_cap() {
 #ifdef QCB_F32_SCALED_CAP                              // tuning experiments: scaled Z only
   if constexpr (ZS > 0 && ZS != S::Z0) return cap > QCB_F32_SCALED_CAP ? QCB_F32_SCALED_CAP : cap;
 #endif
+  // scaled Z: a 128-register cap where the per-code sweep measured it ahead
+  // (4 warps per sub-partition, so CTAs of several codewords stay co-resident)
+  constexpr int kScaled = (ZS > 0 && ZS != S::Z0 && A::kKind == 0) ? scaled_reg_cap(S::ID, 4, ZS) : 0;
+  if constexpr (kScaled > 0) return cap > kScaled ? kScaled : cap;
   return cap > kMax ? kMax : cap;
 }
 
@@ -881,6 +935,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
   const uint32_t cws = (uint32_t)cw_block_bytes(Z);      // bytes per codeword block
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  dbg_check(cw0 < a.w && ncw >= 1 && ncw <= G, 21);           // the CTA's chunk lies inside the batch
+  dbg_poison_smem();
+  dbg_inject_probe(a.dbg_inject, sbase);
   // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
   // warp: same row, same inputs, same instruction stream, so in lockstep they
   // load and store the very words their twins do (same-word accesses: no bank

@@ -70,6 +70,9 @@
 #ifndef QCB_P16_TM_CAP
 #define QCB_P16_TM_CAP 128
 #endif
+#ifndef QCB_P16_TM_WAIT0
+#define QCB_P16_TM_WAIT0 1      // tcgen05.wait::st once per sweep (tier 0) instead of every TMEM tier
+#endif
 constexpr int p16_tmt_default(int id) {
   return (id == 6 || id == 7 || id == 15) ? 3 : ((id == 5 || id == 17) ? 2 : 0);
 }
@@ -118,8 +121,14 @@ struct ArithI16x2 {
   static constexpr int kElem = 4;        // one cell = the two codewords' int16 posteriors
   static constexpr int kKind = 2;        // address-table policy key (use_addr_tab)
 
-  __device__ static Val lds(uint32_t a) { uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
-  __device__ static void sts(uint32_t a, Val v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+  __device__ static Val lds(uint32_t a) {
+    dbg_smem(a, 4, 11);
+    uint32_t v; asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a)); return v;
+  }
+  __device__ static void sts(uint32_t a, Val v) {
+    dbg_smem(a, 4, 12);
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+  }
 
   // One row of D edges: posteriors p[] in, new posteriors o[] out, negated
   // messages nm[] updated in place (both codewords' lanes).
@@ -251,7 +260,11 @@ struct Layered2 {
     uint32_t mt[T < TMT ? D : 1];
     if constexpr (T < TMT) {
       (void)tb;
-      tm_wait_st();                              // this thread's earlier TMEM stores have landed
+      // Tier T reads the columns tier T stored one sweep ago.  One wait at tier
+      // 0 covers every store of the previous sweep; waiting again at tiers 1..
+      // TMT-1 would also wait for the store tier T-1 issued just before the
+      // barrier (ncu, C5: those two waits held 5.8 % of all stall samples).
+      if constexpr (T == 0 || !QCB_P16_TM_WAIT0) tm_wait_st();
       tm_ld_n<E0, D>(tb, mt);                    // overlaps the posterior loads below
     }
     tab_compose<S, A, ZS, TAB, T>(a, r, b0, b1, ec, addr, std::make_integer_sequence<int, D>{});
@@ -421,6 +434,8 @@ constexpr int p16_reg_cap() {
 #ifdef QCB_P16_SCALED_CAP                              // tuning experiments: scaled Z only
   if constexpr (ZS > 0 && ZS != S::Z0) return cap > QCB_P16_SCALED_CAP ? QCB_P16_SCALED_CAP : cap;
 #endif
+  constexpr int kScaled = (ZS > 0 && ZS != S::Z0) ? scaled_reg_cap(S::ID, 2, ZS) : 0;   // see reg_cap
+  if constexpr (kScaled > 0) return cap > kScaled ? kScaled : cap;
   return cap > kMax ? kMax : cap;
 }
 
@@ -447,6 +462,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const int npairs = (ncw + 1) >> 1;
   const uint32_t cws = (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  dbg_check(cw0 < a.w && ncw >= 1 && ncw <= 2 * G, 22);       // the CTA's chunk lies inside the batch
+  dbg_poison_smem();
+  dbg_inject_probe(a.dbg_inject, sbase);
   // Padding lanes of the last warp (tid >= G*Z) shadow real lanes of the SAME
   // warp: same row, same inputs, same instruction stream, so in lockstep they
   // load and store the very words their twins do (same-word accesses: no bank

@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((tm_reg_cap<S, A>(
   const bool act = g < ncw;
   const uint32_t cws = (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  dbg_check(cw0 < a.w && ncw >= 1 && ncw <= G, 23);           // the CTA's chunk lies inside the batch
+  dbg_poison_smem();
+  dbg_inject_probe(a.dbg_inject, sbase);
   uint32_t b0 = sbase + (uint32_t)g * cws + (uint32_t)(r * kCellBytes), b1;
   asm volatile("mov.b32 %0, %0;" : "+r"(b0));
   asm volatile("sub.u32 %0, %1, %2;" : "=r"(b1) : "r"(b0), "r"((uint32_t)(Z * kCellBytes)));

@@ -43,6 +43,7 @@ struct SpecArgs {
   uint32_t k_one, k_sign, k_shr, k_neg1;  // 1, 2^31, 2^31+1, -1: IMAD multipliers kept out of ptxas' reach
   uint32_t k_lane1;   // 0x00010001 (16x2 lane constant)
   int32_t pair16;     // int16 only: 1 = two codewords per thread in 16x2 lanes (pairs = codeword pairs per CTA)
+  int32_t dbg_inject; // debug builds only (QCB_DEBUG_CHECKS): 1 = make one out-of-bounds shared access (negative control)
   int32_t off[kMaxStructEntries];  // per entry: e*RS + j*ES (bytes, relative to the thread's row)
   int32_t thr[kMaxStructEntries];  // per entry: Z - e (row r wraps when r >= thr)
 };

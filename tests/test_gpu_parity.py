@@ -219,11 +219,12 @@ def test_generic_kernel_on_nonstandard_codes():
 
 
 def test_standard_structure_with_foreign_shifts():
-    """A standard zero-block pattern at its native Z but with other shift values
-    must not take the compile-time-shift kernels (decoder and encoder)."""
+    """A standard zero-block pattern at its native Z (or at a scaled WiMAX Z) but with
+    other shift values must not take the compile-time-shift kernels (decoder and
+    encoder): the runtime-Z kernels serve it."""
     rng = np.random.default_rng(17)
     for std, n, rate in (("wimax", 2304, "1/2"), ("wimax", 2304, "3/4A"), ("wifi", 1944, "5/6"),
-                         ("wifi", 648, "1/2")):
+                         ("wifi", 648, "1/2"), ("wimax", 960, "3/4A"), ("wimax", 576, "2/3A")):
         base = P.get_model_matrix(std, n, rate)
         ent = base.entries.copy()
         nz = ent >= 0

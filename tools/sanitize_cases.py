@@ -48,9 +48,13 @@ def main():
     quick = "--quick" in sys.argv
     n_ok = 0
 
-    def dec(mm, w, fixed, early, iters=3, misalign=False, tag=""):
+    def dec(mm, w, fixed, early, iters=3, misalign=False, tag="", random=False):
         nonlocal n_ok
-        llr, _, _ = noisy_llrs(mm, w, 2.5, seed=int(rng.integers(1 << 30)), fixed=fixed)
+        if random:                         # a code without a direct encoder (generic kernel case)
+            v = rng.standard_normal((w, mm.n)) * 3.0
+            llr = P.quantize_llr(v).values if fixed else v.astype(np.float32)
+        else:
+            llr, _, _ = noisy_llrs(mm, w, 2.5, seed=int(rng.integers(1 << 30)), fixed=fixed)
         cfg = P.DecoderConfig(max_iterations=iters, early_termination=early,
                               arithmetic=P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32)
         t = torch.from_numpy(llr).cuda()
@@ -71,7 +75,8 @@ def main():
     cases = [
         (("wimax", 2304, "1/2"), False), (("wifi", 648, "1/2"), False),
         (("wimax", 2304, "3/4A"), True), (("wifi", 1944, "5/6"), True),
-        (("wimax", 960, "3/4A"), False), (("wimax", 960, "3/4A"), True),      # runtime Z (scaled)
+        (("wimax", 960, "3/4A"), False), (("wimax", 960, "3/4A"), True),      # scaled Z (per-Z kernels)
+        (("wimax", 576, "1/2"), True),                                         # int16 Z = 24: CTA barriers
         (("wifi", 1296, "2/3"), True),                                         # Z = 54, global table
     ]
     for code, fixed in cases:
@@ -80,6 +85,15 @@ def main():
             dec(mm, 3, fixed, early, tag=f"{code} fixed={fixed} et={early}")
     dec(P.get_model_matrix("wimax", 2304, "3/4A"), 5, True, False, misalign=True, tag="misaligned int16")
     dec(P.get_model_matrix("wimax", 2304, "1/2"), 3, False, True, misalign=True, tag="misaligned f32")
+    # runtime-Z kernels: a scaled-Z WiMAX structure with foreign shift values
+    base = P.get_model_matrix("wimax", 960, "3/4A")
+    ent = base.entries.copy()
+    nz = ent >= 0
+    ent[nz] = rng.integers(0, base.z, size=int(nz.sum()))
+    ent[:, base.kb:] = base.entries[:, base.kb:]
+    foreign = P.ModelMatrix(base.standard, base.rate, base.z, base.nb, base.kb, ent)
+    for fixed in (False, True):
+        dec(foreign, 5, fixed, True, tag=f"runtime-Z fixed={fixed}")
     # TMEM float32 kernel (the default for scaled degree-20 codes with Z >= 40)
     dec(P.get_model_matrix("wimax", 1152, "5/6"), 3, False, True, tag="tmem f32")
     # generic kernel
@@ -87,7 +101,7 @@ def main():
     ent[:, 0] = rng.integers(0, 17, size=4)
     gen = P.ModelMatrix(P.Standard.Wimax, P.Rate.R12, 17, 10, 6, ent)
     for fixed in (False, True):
-        dec(gen, 3, fixed, True, tag=f"generic fixed={fixed}")
+        dec(gen, 3, fixed, True, tag=f"generic fixed={fixed}", random=True)
 
     # encoders
     for code, w in ((("wimax", 2304, "3/4A"), 300), (("wimax", 2304, "1/2"), 129), (("wimax", 576, "2/3B"), 77)):
