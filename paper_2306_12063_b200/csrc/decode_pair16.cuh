@@ -73,8 +73,10 @@
 #ifndef QCB_P16_TM_WAIT0
 #define QCB_P16_TM_WAIT0 1      // tcgen05.wait::st once per sweep (tier 0) instead of every TMEM tier
 #endif
+// Wi-Fi 1944 R2/3 (5) dropped its TMEM tiers in round 2: without them it packs
+// three pairs per CTA (native_fill_cw), 88.9 -> 93.2 Gb/s (r02_call10.sh).
 constexpr int p16_tmt_default(int id) {
-  return (id == 6 || id == 7 || id == 15) ? 3 : ((id == 5 || id == 17) ? 2 : 0);
+  return (id == 6 || id == 7 || id == 15) ? 3 : (id == 17 ? 2 : 0);
 }
 
 namespace qcb {
@@ -211,6 +213,15 @@ struct Layered2 {
   static constexpr int TMC = S::START[TMT];
   static constexpr int NR = S::NE - TMC;
   static constexpr int TCOLS = TMC <= 32 ? 32 : (TMC <= 64 ? 64 : (TMC <= 128 ? 128 : 256));
+  // several pairs per CTA (fixed iterations): warps w and w + 4 share TMEM
+  // lanes (a warp reaches lanes 32 (w mod 4) ..), so each group of four warps
+  // takes its own TMC columns; the allocation is the next power of two
+  __host__ __device__ static constexpr int tm_cols(int warps) {
+    const int need = ((warps + 3) / 4) * TMC;
+    int c = 32;
+    while (c < need) c *= 2;
+    return c;
+  }
 
   template <int T>
   __device__ __forceinline__ static void fetch(uint32_t tab, uint32_t* ent) {
@@ -487,7 +498,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   if constexpr (L::TMT > 0) {                   // one warp allocates the CTA's message columns
     if (tid < 32) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                   ::"r"((uint32_t)__cvta_generic_to_shared(&s_taddr)), "r"((uint32_t)L::TCOLS));
+                   ::"r"((uint32_t)__cvta_generic_to_shared(&s_taddr)), "r"((uint32_t)L::tm_cols(blockDim.x >> 5)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   uint32_t tb = 0;                              // this thread's TMEM lane, column 0
   if constexpr (L::TMT > 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    tb = s_taddr + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16);
+    tb = s_taddr + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + (uint32_t)((tid >> 7) * L::TMC);
     uint32_t z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // messages start at 0 (reference init)
 #pragma unroll
     for (int c = 0; c + 8 <= L::TMC; c += 8) tm_st<8>(tb + c, z8);
@@ -626,7 +637,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (tid < 32)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "r"((uint32_t)L::TCOLS));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr),
+                   "r"((uint32_t)L::tm_cols(blockDim.x >> 5)));
   }
 }
 
@@ -688,9 +700,16 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   cudaError_t e = kernel_attributes((const void*)kern, &fa);
   if (e != cudaSuccess) return e;
   SpecArgs b = a;
-  b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4, ZS == S::Z0 ? 1 : lane_fill_cw(z, 2, S::ID));
+  b.pairs = layered_cw_per_cta(z, (a.w + 1) / 2, fa.numRegs, 4,
+                               ZS == S::Z0 ? native_fill_cw(2, S::ID) : lane_fill_cw(z, 2, S::ID));
   if constexpr (one_warp_cta<ZS, 2>()) b.pairs = 1;         // tier_sync is a warp barrier
-  if constexpr (Layered2<S, ZS>::GT || Layered2<S, ZS>::TMT > 0) b.pairs = 1;   // per-thread global table / TMEM lanes
+  // per-thread global table: one pair; TMEM tiers: several pairs only with fixed
+  // iterations (the multi-pair early-termination loop skips tiers per pair, and
+  // tcgen05.ld/st are warp-collective)
+  if constexpr (Layered2<S, ZS>::GT) b.pairs = 1;
+  if constexpr (Layered2<S, ZS>::TMT > 0) {
+    if (ET) b.pairs = 1;
+  }
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;

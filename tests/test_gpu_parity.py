@@ -557,7 +557,8 @@ SCALED_Z = list(range(24, 93, 4))
 def test_scaled_codes_compile_time_kernels_at_plan_size_match_oracle(fixed):
     """The 108 scaled WiMAX codes run decoders compiled for their own Z
     (csrc/decode_scaled.cuh) with the measured codewords-per-CTA plan
-    (csrc/scaled_plan_gen.h), which only engages for batches of several waves:
+    (csrc/scaled_plan_gen.h; int16 Wi-Fi 1944 R1/2 and R2/3 too, native_fill_cw),
+    which only engages for batches of several waves:
     10,000 codewords per code here, device channel frames, every code, fixed
     iterations (and early termination on a Z subset), checked against the C
     oracle on sampled rows: the first and last CTAs' codewords (including a
@@ -568,9 +569,11 @@ def test_scaled_codes_compile_time_kernels_at_plan_size_match_oracle(fixed):
     arith = P.Arithmetic.Fixed16 if fixed else P.Arithmetic.Float32
     rng = np.random.default_rng(77 + fixed)
     w = 10_001
-    for ci, (std, n, rate) in enumerate(P.supported_codes()):
-        if std != "wimax" or n == 2304:
-            continue
+    codes = [(s.value, n, r.value) for s, n, r in P.supported_codes() if s.value == "wimax" and n != 2304]
+    assert len(codes) == 108
+    if fixed:       # native int16 codes with a multi-pair plan (native_fill_cw)
+        codes += [("wifi", 1944, "1/2"), ("wifi", 1944, "2/3")]
+    for ci, (std, n, rate) in enumerate(codes):
         mm = P.get_model_matrix(std, n, rate)
         h = P.expand(mm)
         info = CH.frames_info_device(31, ci, 0, w, mm.k, dev)
