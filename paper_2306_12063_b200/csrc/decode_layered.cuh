@@ -1050,12 +1050,14 @@ inline const ScaledPlan* scaled_plan(int structure_id, int elem, int z) {
     if (kScaledPlan[i].id == structure_id && kScaledPlan[i].elem == elem && kScaledPlan[i].z == z) return &kScaledPlan[i];
   return nullptr;
 }
-// The native Z = 81 int16 codes without TMEM tiers: three pairs (243 rows) in
-// eight warps busy 95 % of the lanes where one pair keeps 81 of 96: Wi-Fi 1944
-// R1/2 96.0 -> 102.3, R2/3 88.9 -> 93.2 Gb/s; R5/6 and R3/4 keep one pair
-// with TMEM tiers (round 2, tools/exp/r02_call10.sh); float32 loses with G > 1.
+// The native Z = 81 int16 codes: three pairs (243 rows) in eight warps busy 95 %
+// of the lanes where one pair keeps 81 of 96: Wi-Fi 1944 R1/2 96.0 -> 102.3,
+// R2/3 88.9 -> 93.2 Gb/s (without TMEM tiers), R3/4 89.1 -> 93.1 and R5/6 (C3)
+// 96.1 -> 102.4 (TMEM tiers, one column group per four warps; fixed iterations
+// only) (round 2, tools/exp/r02_call10.sh, r02_call12.sh).  WiMAX (Z = 96, no
+// idle lanes) loses 9-32 % with G > 1, float32 loses everywhere.
 inline int native_fill_cw(int kind, int structure_id) {
-  return (kind == 2 && (structure_id == 4 || structure_id == 5)) ? 3 : 1;
+  return (kind == 2 && structure_id >= 4 && structure_id <= 7) ? 3 : 1;
 }
 inline int lane_fill_cw(int z, int kind, int structure_id) {
   const ScaledPlan* p = scaled_plan(structure_id, kind == 2 ? 2 : 4, z);

@@ -572,7 +572,7 @@ def test_scaled_codes_compile_time_kernels_at_plan_size_match_oracle(fixed):
     codes = [(s.value, n, r.value) for s, n, r in P.supported_codes() if s.value == "wimax" and n != 2304]
     assert len(codes) == 108
     if fixed:       # native int16 codes with a multi-pair plan (native_fill_cw)
-        codes += [("wifi", 1944, "1/2"), ("wifi", 1944, "2/3")]
+        codes += [("wifi", 1944, "1/2"), ("wifi", 1944, "2/3"), ("wifi", 1944, "3/4"), ("wifi", 1944, "5/6")]
     for ci, (std, n, rate) in enumerate(codes):
         mm = P.get_model_matrix(std, n, rate)
         h = P.expand(mm)
