@@ -200,7 +200,9 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
 // pair q's block (n cells) at sbase + 4 q n.  Units of eight cells: two
 // 16-byte loads per codeword keep as many bytes in flight as the float32 path
 // (units of four halved them and cost C5 1.3 %), stored with sts_cells8.
-__device__ __forceinline__ void load_llrs_pair16(const int16_t* chunk, int ncw, int n, uint32_t sbase) {
+// cpad: bytes of padding after each pair's block (several pairs per CTA, p16_block_stride)
+__device__ __forceinline__ void load_llrs_pair16(const int16_t* chunk, int ncw, int n, uint32_t sbase,
+                                                 uint32_t cpad = 0) {
   const int npairs = (ncw + 1) >> 1;
   const int units = npairs * n / 8;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -234,16 +236,16 @@ __device__ __forceinline__ void load_llrs_pair16(const int16_t* chunk, int ncw, 
                                     __byte_perm(x[k].y, y[k].y, 0x5410), __byte_perm(x[k].y, y[k].y, 0x7632));
         const uint4 hi = make_uint4(__byte_perm(x[k].z, y[k].z, 0x5410), __byte_perm(x[k].z, y[k].z, 0x7632),
                                     __byte_perm(x[k].w, y[k].w, 0x5410), __byte_perm(x[k].w, y[k].w, 0x7632));
-        sts_cells8(sbase, u, lo, hi);
+        sts_cells8(sbase + (uint32_t)((8 * u) / n) * cpad, u, lo, hi);
       } else {
-        sts_cells8(sbase, u, x[k], y[k]);
+        sts_cells8(sbase + (uint32_t)((8 * u) / n) * cpad, u, x[k], y[k]);
       }
     }
   }
 }
 
 __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, int16_t* post, int ncw, int n,
-                                                     uint32_t sbase) {
+                                                     uint32_t sbase, uint32_t cpad = 0) {
   const int npairs = (ncw + 1) >> 1;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const bool al = ((reinterpret_cast<uintptr_t>(hard) | reinterpret_cast<uintptr_t>(post)) & 15) == 0;
@@ -256,8 +258,8 @@ __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, 
         const int u = base + k * nthr + tid;
         if (u >= units) continue;
         uint32_t v[8];
-        lds_cells8(sbase, u, v);
         const int e = 8 * u, q = e / n, nn = e - q * n;
+        lds_cells8(sbase + (uint32_t)q * cpad, u, v);
 #pragma unroll
         for (int lane = 0; lane < 2; ++lane) {
           const int cw = 2 * q + lane;
@@ -286,9 +288,9 @@ __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, 
     for (int k = 0; k < kIoUnroll; ++k) {
       const int u = base + k * nthr + tid;
       if (u >= units) continue;
-      const uint4 c = lds128(sbase + 16u * (uint32_t)u);
-      const uint32_t v[4] = {c.x, c.y, c.z, c.w};
       const int e = 4 * u, q = e / n, nn = e - q * n;
+      const uint4 c = lds128(sbase + 16u * (uint32_t)u + (uint32_t)q * cpad);
+      const uint32_t v[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
       for (int lane = 0; lane < 2; ++lane) {
         const int cw = 2 * q + lane;

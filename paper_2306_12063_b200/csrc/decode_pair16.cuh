@@ -450,6 +450,15 @@ constexpr int p16_reg_cap() {
   return cap > kMax ? kMax : cap;
 }
 
+// Bytes between consecutive pair blocks in shared memory: the block itself
+// (24 Z cells), padded to a multiple of 128 bytes (32 banks) when a CTA holds
+// several pairs.  Z = 81: 1944 -> 1952 cells; measured on C3 (three pairs per
+// CTA): shared-memory bank conflicts 25 % -> see DESIGN 3.2.  The scaled WiMAX Z
+// (multiples of 4) are aligned already.
+__host__ __device__ constexpr int p16_block_stride(int z, int pairs) {
+  return pairs > 1 ? (cw_block_bytes(z) + 127) / 128 * 128 : cw_block_bytes(z);
+}
+
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q
 template <class S, int ZS, bool ET>
 __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS>()))
@@ -471,7 +480,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   const int64_t cw0 = (int64_t)blockIdx.x * (2 * G);
   const int ncw = (int)(a.w - cw0 < (int64_t)(2 * G) ? a.w - cw0 : (int64_t)(2 * G));
   const int npairs = (ncw + 1) >> 1;
-  const uint32_t cws = (uint32_t)cw_block_bytes(Z);
+  // pair blocks: with several pairs per CTA the block stride is padded to a
+  // multiple of 32 banks (p16_block_stride), so rows of two pairs in one warp
+  // fall on banks offset only by their cells (C3's Z = 81: 24-bank offset)
+  const uint32_t cws = (uint32_t)p16_block_stride(Z, G);
+  const uint32_t cpad = cws - (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   dbg_check(cw0 < a.w && ncw >= 1 && ncw <= 2 * G, 22);       // the CTA's chunk lies inside the batch
   dbg_poison_smem();
@@ -505,7 +518,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
-    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase);
+    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -630,7 +643,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
   store_outputs_pair16(reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N), a.hard_packed,
-                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, sbase);
+                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, sbase, cpad);
   if constexpr (L::TMT > 0) {                   // release the message columns
     tm_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -713,7 +726,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const size_t cwsb = (size_t)cw_block_bytes(z);
+  const size_t cwsb = (size_t)p16_block_stride(z, b.pairs);
   constexpr int kTabB = Layered2<S, ZS>::GT ? 0 : addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
   const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * kTabB + 15) & ~(size_t)15) +
                       (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block
