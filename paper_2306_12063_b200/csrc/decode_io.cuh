@@ -74,8 +74,9 @@ __device__ __forceinline__ void sts_cells8(uint32_t blk, int u, const uint4& lo,
 // ---- float32: one codeword per 4-byte cell ----------------------------------------
 // LLRs are canonicalised on the way in (v + 0.0f, see ArithF32::canon).
 // The CTA's ncw codewords (ncw * n floats) land at sbase + 4 e.
+// cpad: bytes of padding after each codeword's block (blk_stride_bytes)
 template <bool IO8>
-__device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n, uint32_t sbase) {
+__device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n, uint32_t sbase, uint32_t cpad = 0) {
   const int total = ncw * n;
   const int tid = threadIdx.x, nthr = blockDim.x;
   if ((reinterpret_cast<uintptr_t>(chunk) & 15) == 0) {
@@ -93,7 +94,7 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
         for (int u = 0; u < kIoUnroll; ++u) {
           const int i = base + u * nthr + tid;
           if (i < total4)
-            sts128(sbase + 16u * (uint32_t)i,
+            sts128(sbase + 16u * (uint32_t)i + (cpad ? (uint32_t)((4 * i) / n) * cpad : 0u),
                    make_uint4(__float_as_uint(__fadd_rn(v[u].x, 0.0f)), __float_as_uint(__fadd_rn(v[u].y, 0.0f)),
                               __float_as_uint(__fadd_rn(v[u].z, 0.0f)), __float_as_uint(__fadd_rn(v[u].w, 0.0f))));
         }
@@ -112,7 +113,7 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
       for (int u = 0; u < kIoUnroll; ++u) {
         const int i = base + u * nthr + tid;
         if (i < units)
-          sts_cells8(sbase, i,
+          sts_cells8(sbase + (cpad ? (uint32_t)((8 * i) / n) * cpad : 0u), i,
                      make_uint4(__float_as_uint(__fadd_rn(v[u].x, 0.0f)), __float_as_uint(__fadd_rn(v[u].y, 0.0f)),
                                 __float_as_uint(__fadd_rn(v[u].z, 0.0f)), __float_as_uint(__fadd_rn(v[u].w, 0.0f))),
                      make_uint4(__float_as_uint(__fadd_rn(w[u].x, 0.0f)), __float_as_uint(__fadd_rn(w[u].y, 0.0f)),
@@ -120,7 +121,9 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
       }
     }
   } else {
-    for (int e = tid; e < total; e += nthr) sts32(sbase + 4u * (uint32_t)e, __float_as_uint(__fadd_rn(__ldcs(chunk + e), 0.0f)));
+    for (int e = tid; e < total; e += nthr)
+      sts32(sbase + 4u * (uint32_t)e + (cpad ? (uint32_t)(e / n) * cpad : 0u),
+            __float_as_uint(__fadd_rn(__ldcs(chunk + e), 0.0f)));
   }
 }
 
@@ -128,7 +131,8 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
 // packed (np.packbits, MSB first); optional float32 posteriors
 template <bool IO8, class HardFn, class PostFn>
 __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, float* post, int ncw, int n,
-                                                     uint32_t sbase, HardFn is_hard, PostFn post_bits) {
+                                                     uint32_t sbase, HardFn is_hard, PostFn post_bits,
+                                                     uint32_t cpad = 0) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const bool al = ((reinterpret_cast<uintptr_t>(hard) | reinterpret_cast<uintptr_t>(post)) & 15) == 0;
   if (!IO8 && !packed) {                                 // 4 consecutive cells per unit
@@ -138,7 +142,7 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
       for (int k = 0; k < kIoUnroll; ++k) {
         const int u = base + k * nthr + tid;
         if (u >= units4) continue;
-        const uint4 c = lds128(sbase + 16u * (uint32_t)u);
+        const uint4 c = lds128(sbase + 16u * (uint32_t)u + (cpad ? (uint32_t)((4 * u) / n) * cpad : 0u));
         const uint32_t v[4] = {c.x, c.y, c.z, c.w};
         uint32_t word = 0;
 #pragma unroll
@@ -163,7 +167,7 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
       const int u = base + k * nthr + tid;
       if (u >= units) continue;
       uint32_t v[8];
-      lds_cells8(sbase, u, v);
+      lds_cells8(sbase + (cpad ? (uint32_t)((8 * u) / n) * cpad : 0u), u, v);
       const int e = 8 * u;
       if (packed) {
         uint32_t byte = 0;

@@ -73,10 +73,38 @@ constexpr int kLayMaxCw = 16;
 // residues W k mod 32 are distinct (W odd): no bank conflicts, where 32
 // consecutive rows wrapping at Z put up to two lanes on one bank.  Padding
 // lanes shadow a real lane of the same warp (same row, same words, lockstep).
+//
+// Several codewords per CTA whose count G divides 32 and with m = 32 / G
+// dividing Z ("chunked"): lane l of warp w takes row w m + (l mod m) of
+// codeword l / m, and consecutive codeword blocks sit m banks apart
+// (blk_stride_bytes).  Every lane of a warp then reads the same m cells
+// (consecutive mod Z, so distinct mod m) of its own codeword, at bank
+// (g m + c) mod 32: conflict-free for every shift, no idle lanes, Z / m warps
+// (Z = 24, 40: G = 4; 48, 80: G = 2).  The contiguous mapping of several
+// codewords put up to 0.5-1 extra wavefronts on every access (bank model over
+// all shifts; ncu: 33 % of WiMAX 864 R3/4A's shared wavefronts).
 struct RowMap {
   int g, r;
 };
+__host__ __device__ constexpr int chunk_m(int Z, int G) {
+  return (G > 1 && 32 % G == 0 && Z % (32 / G) == 0) ? 32 / G : 0;
+}
+// bytes between consecutive codeword (pair) blocks in shared memory: the block
+// (24 Z cells), offset to m banks for the chunked mapping, or (align32, several
+// blocks) padded to a multiple of 32 banks
+__host__ __device__ constexpr int blk_stride_bytes(int Z, int G, bool align32) {
+  const int w = 24 * Z;
+  return chunk_m(Z, G) ? 4 * (w + ((chunk_m(Z, G) - w % 32) % 32 + 32) % 32)
+                       : ((align32 && G > 1) ? 4 * ((w + 31) / 32 * 32) : 4 * w);
+}
+#ifndef QCB_CHUNKED_ROWS
+#define QCB_CHUNKED_ROWS 1
+#endif
 __device__ __forceinline__ RowMap map_row(int tid, int G, int Z) {
+  if (QCB_CHUNKED_ROWS && chunk_m(Z, G)) {
+    const int m = chunk_m(Z, G), lane = tid & 31;
+    return RowMap{lane / m, (tid >> 5) * m + lane % m};
+  }
   const int W = (Z + 31) >> 5;
   if (G == 1 && W > 1 && (W & 1) && Z % W == 0) {
     const int per = Z / W, lane = tid & 31;
@@ -933,7 +961,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int g = tid / Z, r = tid - g * Z;
   const int64_t cw0 = (int64_t)blockIdx.x * G;
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
-  const uint32_t cws = (uint32_t)cw_block_bytes(Z);      // bytes per codeword block
+  const uint32_t cws = (uint32_t)blk_stride_bytes(Z, G, false);   // bytes per codeword block (+ bank offset)
+  const uint32_t cpad = cws - (uint32_t)cw_block_bytes(Z);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   dbg_check(cw0 < a.w && ncw >= 1 && ncw <= G, 21);           // the CTA's chunk lies inside the batch
   dbg_poison_smem();
@@ -962,7 +991,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 
   // ---- channel LLRs -> the codewords' blocks (bit order) ----------------------
   {
-    load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase);
+    load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -1034,7 +1063,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
   store_outputs_cell32<io_cells8<ZS>()>(hard, a.hard_packed, post, ncw, N, sbase,
                        [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
-                       [](uint32_t v) { return __uint_as_float(v); });
+                       [](uint32_t v) { return __uint_as_float(v); }, cpad);
 }
 
 // codewords per CTA for a kernel with `regs` registers per thread
@@ -1042,9 +1071,11 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 // last warp idle (the scaled WiMAX codes): G codewords' rows are dealt out
 // contiguously over ceil(G Z / 32) warps, so a G with G Z near a multiple of
 // 32 busies more lanes, at the price of a tier barrier over more warps.
-// Measured per scaled code for G = 1..4 (scaled_plan_gen.h): Z = 36, 40 take
-// G = 3 (+25-39 %), Z = 44, 48 G = 2 (+15-23 %), Z = 68-84 G = 3 on the
-// lower-degree structures; full or nearly full Z keep G = 1.
+// Measured per scaled code for G = 1, 2, 3, 4, 8 (scaled_plan_gen.h): G = 2
+// or 4 where the chunked mapping applies (Z = 24, 40, 48, 80: conflict-free,
+// no idle lanes; float32 WiMAX 960 R2/3B 55.0 -> 68.2, 1152 R3/4A 54.7 -> 67.8
+// Gb/s), G = 3 at Z = 36 and on the lower-degree structures at Z = 68-84;
+// full or nearly full Z keep G = 1.
 inline const ScaledPlan* scaled_plan(int structure_id, int elem, int z) {
   for (int i = 0; i < kScaledPlans; ++i)
     if (kScaledPlan[i].id == structure_id && kScaledPlan[i].elem == elem && kScaledPlan[i].z == z) return &kScaledPlan[i];
@@ -1079,9 +1110,10 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes, int fi
 
 template <class K>
 inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, cudaStream_t s, int tab_bytes = 0,
-                                        int msg_bytes = 0) {
+                                        int msg_bytes = 0, int blk_bytes = 0) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
-  const size_t smem = (((size_t)a.pairs * cw_block_bytes(z) + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
+  const size_t blk = blk_bytes > 0 ? (size_t)blk_bytes : (size_t)cw_block_bytes(z);
+  const size_t smem = (((size_t)a.pairs * blk + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
                       (size_t)threads * msg_bytes;
   cudaError_t e = ensure_dyn_smem((const void*)kern, smem);
   if (e != cudaSuccess) return e;
@@ -1106,7 +1138,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   return launch_layered_fixed(kern, b, z, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
-                              SmemMsg<S>::words() * 4);
+                              SmemMsg<S>::words() * 4, blk_stride_bytes(z, b.pairs, false));
 }
 
 }  // namespace qcb

@@ -456,7 +456,7 @@ constexpr int p16_reg_cap() {
 // CTA): shared-memory bank conflicts 25 % -> see DESIGN 3.2.  The scaled WiMAX Z
 // (multiples of 4) are aligned already.
 __host__ __device__ constexpr int p16_block_stride(int z, int pairs) {
-  return pairs > 1 ? (cw_block_bytes(z) + 127) / 128 * 128 : cw_block_bytes(z);
+  return blk_stride_bytes(z, pairs, true);     // chunked pairs: m banks apart (map_row)
 }
 
 // a.pairs = codeword PAIRS per CTA; codeword 2q of the CTA is lane 0 of pair q

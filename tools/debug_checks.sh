@@ -20,3 +20,5 @@ timeout 900 python tools/sanitize_cases.py > gpurun_out/debug_sanitize_cases.log
 echo "debug sanitize_cases rc=$?"; tail -2 gpurun_out/debug_sanitize_cases.log
 QCB_CW_PER_CTA=3 timeout 900 python tools/sanitize_cases.py > gpurun_out/debug_sanitize_cases_g3.log 2>&1
 echo "debug sanitize_cases (3 codewords / pairs per CTA) rc=$?"; tail -2 gpurun_out/debug_sanitize_cases_g3.log
+QCB_CW_PER_CTA=4 timeout 900 python tools/sanitize_cases.py > gpurun_out/debug_sanitize_cases_g4.log 2>&1
+echo "debug sanitize_cases (4 codewords / pairs per CTA: chunked row mapping where 8 | Z) rc=$?"; tail -2 gpurun_out/debug_sanitize_cases_g4.log
