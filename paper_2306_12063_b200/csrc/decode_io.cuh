@@ -75,7 +75,7 @@ __device__ __forceinline__ void sts_cells8(uint32_t blk, int u, const uint4& lo,
 // LLRs are canonicalised on the way in (v + 0.0f, see ArithF32::canon).
 // The CTA's ncw codewords (ncw * n floats) land at sbase + 4 e.
 // cpad: bytes of padding after each codeword's block (blk_stride_bytes)
-template <bool IO8>
+template <bool IO8, bool PAD = false>
 __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n, uint32_t sbase, uint32_t cpad = 0) {
   const int total = ncw * n;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -94,7 +94,7 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
         for (int u = 0; u < kIoUnroll; ++u) {
           const int i = base + u * nthr + tid;
           if (i < total4)
-            sts128(sbase + 16u * (uint32_t)i + (cpad ? (uint32_t)((4 * i) / n) * cpad : 0u),
+            sts128(sbase + 16u * (uint32_t)i + (PAD ? (uint32_t)((4 * i) / n) * cpad : 0u),
                    make_uint4(__float_as_uint(__fadd_rn(v[u].x, 0.0f)), __float_as_uint(__fadd_rn(v[u].y, 0.0f)),
                               __float_as_uint(__fadd_rn(v[u].z, 0.0f)), __float_as_uint(__fadd_rn(v[u].w, 0.0f))));
         }
@@ -113,7 +113,7 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
       for (int u = 0; u < kIoUnroll; ++u) {
         const int i = base + u * nthr + tid;
         if (i < units)
-          sts_cells8(sbase + (cpad ? (uint32_t)((8 * i) / n) * cpad : 0u), i,
+          sts_cells8(sbase + (PAD ? (uint32_t)((8 * i) / n) * cpad : 0u), i,
                      make_uint4(__float_as_uint(__fadd_rn(v[u].x, 0.0f)), __float_as_uint(__fadd_rn(v[u].y, 0.0f)),
                                 __float_as_uint(__fadd_rn(v[u].z, 0.0f)), __float_as_uint(__fadd_rn(v[u].w, 0.0f))),
                      make_uint4(__float_as_uint(__fadd_rn(w[u].x, 0.0f)), __float_as_uint(__fadd_rn(w[u].y, 0.0f)),
@@ -122,14 +122,14 @@ __device__ __forceinline__ void load_llrs_f32(const float* chunk, int ncw, int n
     }
   } else {
     for (int e = tid; e < total; e += nthr)
-      sts32(sbase + 4u * (uint32_t)e + (cpad ? (uint32_t)(e / n) * cpad : 0u),
+      sts32(sbase + 4u * (uint32_t)e + (PAD ? (uint32_t)(e / n) * cpad : 0u),
             __float_as_uint(__fadd_rn(__ldcs(chunk + e), 0.0f)));
   }
 }
 
 // hard decisions (post <= 0) of ncw codewords: unpacked (n bytes each) or
 // packed (np.packbits, MSB first); optional float32 posteriors
-template <bool IO8, class HardFn, class PostFn>
+template <bool IO8, bool PAD = false, class HardFn, class PostFn>
 __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, float* post, int ncw, int n,
                                                      uint32_t sbase, HardFn is_hard, PostFn post_bits,
                                                      uint32_t cpad = 0) {
@@ -142,7 +142,7 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
       for (int k = 0; k < kIoUnroll; ++k) {
         const int u = base + k * nthr + tid;
         if (u >= units4) continue;
-        const uint4 c = lds128(sbase + 16u * (uint32_t)u + (cpad ? (uint32_t)((4 * u) / n) * cpad : 0u));
+        const uint4 c = lds128(sbase + 16u * (uint32_t)u + (PAD ? (uint32_t)((4 * u) / n) * cpad : 0u));
         const uint32_t v[4] = {c.x, c.y, c.z, c.w};
         uint32_t word = 0;
 #pragma unroll
@@ -167,7 +167,7 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
       const int u = base + k * nthr + tid;
       if (u >= units) continue;
       uint32_t v[8];
-      lds_cells8(sbase + (cpad ? (uint32_t)((8 * u) / n) * cpad : 0u), u, v);
+      lds_cells8(sbase + (PAD ? (uint32_t)((8 * u) / n) * cpad : 0u), u, v);
       const int e = 8 * u;
       if (packed) {
         uint32_t byte = 0;
@@ -205,6 +205,7 @@ __device__ __forceinline__ void store_outputs_cell32(uint8_t* hard, int packed, 
 // 16-byte loads per codeword keep as many bytes in flight as the float32 path
 // (units of four halved them and cost C5 1.3 %), stored with sts_cells8.
 // cpad: bytes of padding after each pair's block (several pairs per CTA, p16_block_stride)
+template <bool PAD = false>
 __device__ __forceinline__ void load_llrs_pair16(const int16_t* chunk, int ncw, int n, uint32_t sbase,
                                                  uint32_t cpad = 0) {
   const int npairs = (ncw + 1) >> 1;
@@ -240,14 +241,15 @@ __device__ __forceinline__ void load_llrs_pair16(const int16_t* chunk, int ncw, 
                                     __byte_perm(x[k].y, y[k].y, 0x5410), __byte_perm(x[k].y, y[k].y, 0x7632));
         const uint4 hi = make_uint4(__byte_perm(x[k].z, y[k].z, 0x5410), __byte_perm(x[k].z, y[k].z, 0x7632),
                                     __byte_perm(x[k].w, y[k].w, 0x5410), __byte_perm(x[k].w, y[k].w, 0x7632));
-        sts_cells8(sbase + (uint32_t)((8 * u) / n) * cpad, u, lo, hi);
+        sts_cells8(sbase + (PAD ? (uint32_t)((8 * u) / n) * cpad : 0u), u, lo, hi);
       } else {
-        sts_cells8(sbase + (uint32_t)((8 * u) / n) * cpad, u, x[k], y[k]);
+        sts_cells8(sbase + (PAD ? (uint32_t)((8 * u) / n) * cpad : 0u), u, x[k], y[k]);
       }
     }
   }
 }
 
+template <bool PAD = false>
 __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, int16_t* post, int ncw, int n,
                                                      uint32_t sbase, uint32_t cpad = 0) {
   const int npairs = (ncw + 1) >> 1;
@@ -263,7 +265,7 @@ __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, 
         if (u >= units) continue;
         uint32_t v[8];
         const int e = 8 * u, q = e / n, nn = e - q * n;
-        lds_cells8(sbase + (uint32_t)q * cpad, u, v);
+        lds_cells8(sbase + (PAD ? (uint32_t)q * cpad : 0u), u, v);
 #pragma unroll
         for (int lane = 0; lane < 2; ++lane) {
           const int cw = 2 * q + lane;
@@ -293,7 +295,7 @@ __device__ __forceinline__ void store_outputs_pair16(uint8_t* hard, int packed, 
       const int u = base + k * nthr + tid;
       if (u >= units) continue;
       const int e = 4 * u, q = e / n, nn = e - q * n;
-      const uint4 c = lds128(sbase + 16u * (uint32_t)u + (uint32_t)q * cpad);
+      const uint4 c = lds128(sbase + 16u * (uint32_t)u + (PAD ? (uint32_t)q * cpad : 0u));
       const uint32_t v[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
       for (int lane = 0; lane < 2; ++lane) {

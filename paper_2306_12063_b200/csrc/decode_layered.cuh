@@ -100,8 +100,8 @@ __host__ __device__ constexpr int blk_stride_bytes(int Z, int G, bool align32) {
 #ifndef QCB_CHUNKED_ROWS
 #define QCB_CHUNKED_ROWS 1
 #endif
-__device__ __forceinline__ RowMap map_row(int tid, int G, int Z) {
-  if (QCB_CHUNKED_ROWS && chunk_m(Z, G)) {
+__device__ __forceinline__ RowMap map_row(int tid, int G, int Z, bool chunked = true) {
+  if (QCB_CHUNKED_ROWS && chunked && chunk_m(Z, G)) {
     const int m = chunk_m(Z, G), lane = tid & 31;
     return RowMap{lane / m, (tid >> 5) * m + lane % m};
   }
@@ -961,8 +961,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   const int g = tid / Z, r = tid - g * Z;
   const int64_t cw0 = (int64_t)blockIdx.x * G;
   const int ncw = (int)(a.w - cw0 < (int64_t)G ? a.w - cw0 : (int64_t)G);
-  const uint32_t cws = (uint32_t)blk_stride_bytes(Z, G, false);   // bytes per codeword block (+ bank offset)
-  const uint32_t cpad = cws - (uint32_t)cw_block_bytes(Z);
+  // bank-offset block stride + chunked rows for the scaled Z only: the native
+  // kernels keep compile-time strides (a runtime pad kept live across the sweep
+  // loop cost C2 1.6 % at the 128-register cap)
+  constexpr bool kPad = ZS != S::Z0;
+  const uint32_t cws = kPad ? (uint32_t)blk_stride_bytes(Z, G, false) : (uint32_t)cw_block_bytes(Z);
+  const uint32_t cpad = kPad ? cws - (uint32_t)cw_block_bytes(Z) : 0u;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   dbg_check(cw0 < a.w && ncw >= 1 && ncw <= G, 21);           // the CTA's chunk lies inside the batch
   dbg_poison_smem();
@@ -973,7 +977,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   // conflict, identical values).  A separate scratch block costs a 2-way bank
   // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
   // shared-memory wavefronts).
-  const RowMap rm = map_row(tid, G, Z);
+  const RowMap rm = map_row(tid, G, Z, kPad);
   const int gs = rm.g, rs = rm.r;
   const bool act = gs < ncw;
   // opaque copies keep the row bases in registers (no per-tier rematerialisation)
@@ -991,7 +995,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
 
   // ---- channel LLRs -> the codewords' blocks (bit order) ----------------------
   {
-    load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
+    if (kPad && cpad) load_llrs_f32<io_cells8<ZS>(), true>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
+    else load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase);
     for (int q = tid; q < kLayMaxCw; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -1061,9 +1066,10 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   }
   uint8_t* hard = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
   float* post = a.post ? reinterpret_cast<float*>(a.post) + cw0 * N : nullptr;
-  store_outputs_cell32<io_cells8<ZS>()>(hard, a.hard_packed, post, ncw, N, sbase,
-                       [](uint32_t v) { return __uint_as_float(v) <= 0.0f; },
-                       [](uint32_t v) { return __uint_as_float(v); }, cpad);
+  const auto is_hard = [](uint32_t v) { return __uint_as_float(v) <= 0.0f; };
+  const auto post_bits = [](uint32_t v) { return __uint_as_float(v); };
+  if (kPad && cpad) store_outputs_cell32<io_cells8<ZS>(), true>(hard, a.hard_packed, post, ncw, N, sbase, is_hard, post_bits, cpad);
+  else store_outputs_cell32<io_cells8<ZS>()>(hard, a.hard_packed, post, ncw, N, sbase, is_hard, post_bits);
 }
 
 // codewords per CTA for a kernel with `regs` registers per thread
@@ -1138,7 +1144,8 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   return launch_layered_fixed(kern, b, z, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
-                              SmemMsg<S>::words() * 4, blk_stride_bytes(z, b.pairs, false));
+                              SmemMsg<S>::words() * 4,
+                              ZS != S::Z0 ? blk_stride_bytes(z, b.pairs, false) : cw_block_bytes(z));
 }
 
 }  // namespace qcb

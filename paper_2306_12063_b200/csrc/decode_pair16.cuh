@@ -483,8 +483,9 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   // pair blocks: with several pairs per CTA the block stride is padded to a
   // multiple of 32 banks (p16_block_stride), so rows of two pairs in one warp
   // fall on banks offset only by their cells (C3's Z = 81: 24-bank offset)
-  const uint32_t cws = (uint32_t)p16_block_stride(Z, G);
-  const uint32_t cpad = cws - (uint32_t)cw_block_bytes(Z);
+  constexpr bool kPad = ZS != S::Z0 || ZS % 32 != 0;   // WiMAX native: compile-time stride (see decode_layered)
+  const uint32_t cws = kPad ? (uint32_t)p16_block_stride(Z, G) : (uint32_t)cw_block_bytes(Z);
+  const uint32_t cpad = kPad ? cws - (uint32_t)cw_block_bytes(Z) : 0u;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   dbg_check(cw0 < a.w && ncw >= 1 && ncw <= 2 * G, 22);       // the CTA's chunk lies inside the batch
   dbg_poison_smem();
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
   // conflict, identical values).  A separate scratch block costs a 2-way bank
   // conflict on every access of that warp (measured: 48 % of Wi-Fi 648's
   // shared-memory wavefronts).
-  const RowMap rm = map_row(tid, G, Z);
+  const RowMap rm = map_row(tid, G, Z, kPad);
   const int gs = rm.g, rs = rm.r;
   const bool act = gs < npairs;
   uint32_t b0 = sbase + (uint32_t)gs * cws + (uint32_t)(rs * kCellBytes), b1;
@@ -518,7 +519,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
 
   // ---- channel LLRs of codewords 2q, 2q+1 -> lanes of [pair][c][j] ----------
   {
-    load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
+    if (kPad && cpad) load_llrs_pair16<true>(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
+    else load_llrs_pair16(reinterpret_cast<const int16_t*>(a.llr) + cw0 * N, ncw, N, sbase);
     for (int q = tid; q < MAXC + 2; q += blockDim.x) {
       s_fail[q] = 1; s_done[q] = q >= ncw; s_iters[q] = 0;
     }
@@ -642,8 +644,12 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((p16_reg_cap<S, ZS
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
   }
-  store_outputs_pair16(reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N), a.hard_packed,
-                       a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr, ncw, N, sbase, cpad);
+  {
+    uint8_t* hard_out = reinterpret_cast<uint8_t*>(a.hard) + cw0 * (a.hard_packed ? (N + 7) >> 3 : N);
+    int16_t* post_out = a.post ? reinterpret_cast<int16_t*>(a.post) + cw0 * N : nullptr;
+    if (kPad && cpad) store_outputs_pair16<true>(hard_out, a.hard_packed, post_out, ncw, N, sbase, cpad);
+    else store_outputs_pair16(hard_out, a.hard_packed, post_out, ncw, N, sbase);
+  }
   if constexpr (L::TMT > 0) {                   // release the message columns
     tm_wait_st();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -726,7 +732,7 @@ inline cudaError_t launch_pair16(const SpecArgs& a, cudaStream_t s) {
   while (b.pairs > 1 && (b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) --b.pairs;
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   const int thr = (b.pairs * z + 31) / 32 * 32;
-  const size_t cwsb = (size_t)p16_block_stride(z, b.pairs);
+  const size_t cwsb = (ZS != S::Z0 || ZS % 32 != 0) ? (size_t)p16_block_stride(z, b.pairs) : (size_t)cw_block_bytes(z);
   constexpr int kTabB = Layered2<S, ZS>::GT ? 0 : addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, ArithI16x2>()>();
   const size_t smem = (((size_t)b.pairs * cwsb + (size_t)thr * kTabB + 15) & ~(size_t)15) +
                       (ET && b.pairs == 1 ? cwsb : 0);   // + snapshot block

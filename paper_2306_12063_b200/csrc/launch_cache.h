@@ -7,6 +7,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -89,5 +90,6 @@ inline cudaError_t kernel_occupancy(const void* k, int threads, size_t smem, int
   *out = f.occ;
   return cudaSuccess;
 }
+
 
 }  // namespace qcb
