@@ -248,9 +248,15 @@ class CopyPool {
 
  private:
   CopyPool() {
+    // every hardware thread of this process's share of the host (the caller is
+    // blocked in the call anyway): measured on C5's pageable e2e (16 threads on
+    // the GPU box): 4 / 8 / 12 / 16 copy threads 9.4 / 14.3 / 17.7 / 19.0 Gbit/s;
+    // torchrun's LOCAL_WORLD_SIZE ranks on one host split the threads
     const char* v = getenv("QCB_COPY_THREADS");
+    const char* lw = getenv("LOCAL_WORLD_SIZE");
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    nthreads_ = v ? std::max(1, atoi(v)) : (int)std::min(16u, std::max(1u, hw / 2));
+    const unsigned ranks = lw ? (unsigned)std::max(1, atoi(lw)) : 1u;
+    nthreads_ = v ? std::max(1, atoi(v)) : (int)std::min(64u, std::max(1u, hw / ranks));
     for (int i = 1; i < nthreads_; ++i) std::thread([this] { loop(); }).detach();
   }
   void drain() {
