@@ -78,6 +78,11 @@ def full(rep: str, config: str, out: str) -> None:
     data = json.loads(p.read_text()) if p.exists() else {}
     main = max(recs, key=lambda r: r["duration_ms"] if isinstance(r["duration_ms"], float) else 0)
     data[config] = dict(main, source=Path(rep).name, launches_captured=len(recs))
+    if "--sum" in sys.argv and len(recs) > 1:
+        # one step = several kernels (C4: one grouped call, 18 codes): traffic and time summed
+        data[config]["dram_bytes_per_launch"] = sum(r.get("dram_bytes_per_launch", 0.0) for r in recs)
+        data[config]["duration_ms_sum"] = sum(r["duration_ms"] for r in recs if isinstance(r["duration_ms"], float))
+        data[config]["note"] = f"dram bytes summed over the {len(recs)} kernels of one step; stats of the longest"
     p.write_text(json.dumps(data, indent=1) + "\n")
     print(json.dumps(data[config], indent=1))
 
