@@ -286,6 +286,14 @@ def cpu_plan(dec, wl, seconds_per_call):
     return plan
 
 
+def physical_cores():
+    try:
+        import psutil
+        return psutil.cpu_count(logical=False)
+    except Exception:  # pragma: no cover - psutil is in the image
+        return None
+
+
 def cpu_baseline(wl, seconds):
     """Best of 3 timed decodes of a bounded sample (rank 0, N=1)."""
     threads = os.cpu_count() or 1
@@ -300,7 +308,8 @@ def cpu_baseline(wl, seconds):
         best = dt if best is None else min(best, dt)
     bits = sum(llr.shape[0] * llr.shape[1] for _, llr in plan)
     sample = "; ".join(f"{code_name(c)}: {llr.shape[0]} codewords" for c, llr in plan)
-    return {"value": round(bits / best / 1e9, 6), "unit": "Gbit/s", "cores": threads, "kind": dec.kind,
+    return {"value": round(bits / best / 1e9, 6), "unit": "Gbit/s", "cores": threads,
+            "physical_cores": physical_cores(), "kind": dec.kind,
             "sample": f"{sample}; best of 3 in {best:.2f} s; {dec.describe()}"}
 
 
@@ -338,7 +347,8 @@ def run_reference(args, wl):
         "higher_is_better": True, "scaling": "strong" if wl.strong else "weak", "vs_baseline": None,
         "dtype": "int16" if wl.fixed else "f32", "data": "synthetic (seeded BPSK/AWGN, reference recipe)",
         "config": cfg,
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads, "kind": dec.kind,
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads,
+                         "physical_cores": physical_cores(), "kind": dec.kind,
                          "sample": f"{sample} per step; {dec.describe()}"},
         "e2e": {"value": round(value, 6), "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
