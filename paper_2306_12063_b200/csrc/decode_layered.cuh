@@ -994,6 +994,10 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   for (int q = 0; q < SmemMsg<S>::words() / 4; ++q) sts128f(mbase + 16u * q, 0.0f, 0.0f, 0.0f, 0.0f);
 
   // ---- channel LLRs -> the codewords' blocks (bit order) ----------------------
+  // Programmatic dependent launch (launch_layered_fixed): nothing above touches
+  // global memory; wait here for the previous kernel of the stream, and let the
+  // next one start its own setup (a no-op pair for an ordinary launch).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     if (kPad && cpad) load_llrs_f32<io_cells8<ZS>(), true>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase, cpad);
     else load_llrs_f32<io_cells8<ZS>()>(reinterpret_cast<const float*>(a.llr) + cw0 * N, ncw, N, sbase);
@@ -1060,6 +1064,8 @@ __global__ void __launch_bounds__(kLayMaxThreads) __maxnreg__((reg_cap<S, A, ZS>
   }
 
   // ---- outputs: iterations, converged, hard decisions, posteriors -------------
+  // (the next launch of the stream may begin its setup while this grid stores its outputs)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid < ncw) {
     a.iters[cw0 + tid] = s_iters[tid];
     a.conv[cw0 + tid] = (a.max_iters > 0 && !s_fail[tid]) ? 1 : 0;
@@ -1116,7 +1122,7 @@ inline int layered_cw_per_cta(int z, int64_t w, int regs, int cell_bytes, int fi
 
 template <class K>
 inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, cudaStream_t s, int tab_bytes = 0,
-                                        int msg_bytes = 0, int blk_bytes = 0) {
+                                        int msg_bytes = 0, int blk_bytes = 0, bool kernel_waits = false) {
   const int threads = (a.pairs * z + 31) / 32 * 32;
   const size_t blk = blk_bytes > 0 ? (size_t)blk_bytes : (size_t)cw_block_bytes(z);
   const size_t smem = (((size_t)a.pairs * blk + (size_t)threads * tab_bytes + 15) & ~(size_t)15) +
@@ -1125,6 +1131,30 @@ inline cudaError_t launch_layered_fixed(K kern, const SpecArgs& a, int z, cudaSt
   if (e != cudaSuccess) return e;
   const int64_t blocks = (a.w + a.pairs - 1) / a.pairs;
   if (blocks <= 0) return cudaSuccess;
+  // Small batches (a grid of at most a few CTAs per SM, BASELINE C1) are launched
+  // with programmatic stream serialization: the grid may start while the previous
+  // kernel of the stream drains, runs its address setup, and blocks at
+  // griddepcontrol.wait (before its first global access) until that kernel has
+  // completed and flushed -- stream order as the caller sees it is unchanged.
+  // C1 (1024 codewords, back-to-back launches): QCB_PDL=0/1, see DESIGN 3.1.
+  static const bool pdl = [] {
+    const char* e = getenv("QCB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  // (kernel_waits: only kernels that execute griddepcontrol.wait may be launched this way)
+  if (pdl && kernel_waits && blocks <= (int64_t)device_sm_count() * 16) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+  }
   kern<<<(unsigned)blocks, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1145,7 +1175,7 @@ inline cudaError_t launch_layered(const SpecArgs& a, cudaStream_t s) {
   if ((b.pairs * z + 31) / 32 * 32 > fa.maxThreadsPerBlock) return cudaErrorLaunchOutOfResources;
   return launch_layered_fixed(kern, b, z, s, addr_tab_bytes_per_thread<S, ZS, use_addr_tab<S, A>()>(),
                               SmemMsg<S>::words() * 4,
-                              ZS != S::Z0 ? blk_stride_bytes(z, b.pairs, false) : cw_block_bytes(z));
+                              ZS != S::Z0 ? blk_stride_bytes(z, b.pairs, false) : cw_block_bytes(z), true);
 }
 
 }  // namespace qcb

@@ -591,3 +591,30 @@ def test_scaled_codes_compile_time_kernels_at_plan_size_match_oracle(fixed):
             assert np.array_equal(it[sel].cpu().numpy(), oi) and np.array_equal(conv[sel].cpu().numpy(), oc), (n, rate)
             assert _post_equal(post[sel].cpu().numpy(), op), (n, rate, early)
         del llr, info
+
+
+@pytest.mark.parametrize("rate", ["1/2", "2/3", "3/4", "5/6"])
+def test_one_warp_cta_codes_small_and_multi_wave_batches_match_oracle(rate):
+    """Wi-Fi 648 float32 (Z = 27, one-warp CTAs with __syncwarp tier barriers and
+    shadow lanes; BASELINE C1's code): a small batch and one of several waves against
+    the C oracle: fixed iterations and early termination, noisy frames plus hostile
+    values (+-0.0, +-inf, NaN, huge, denormal), packed hard bits and posteriors."""
+    mm = P.get_model_matrix("wifi", 648, rate)
+    h = P.expand(mm)
+    for w, seed in ((37, 900), (3001, 901)):
+        llr, _, _ = noisy_llrs(mm, w, 1.0 + 2.0 * mm.rate.fraction, seed=seed + int(mm.rate.fraction * 100))
+        rng = np.random.default_rng(seed)
+        bad = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 3e38, -3e38, 1e-45], np.float32)
+        for row in range(0, min(w, 12)):                      # rows 0..11: sprinkled to all-hostile
+            k = (row + 1) * mm.n // 12
+            idx = rng.choice(mm.n, size=k, replace=False)
+            llr[row, idx] = bad[rng.integers(0, len(bad), size=k)]
+        for early in (False, True):
+            cfg = P.DecoderConfig(max_iterations=7, early_termination=early)
+            hard, it, conv, post = _gpu(mm, llr, cfg)
+            oh, oi, oc, op = O.decode_batch(h, llr, 7, early, workers=4, want_post=True)
+            assert np.array_equal(hard, oh), (rate, w, early)
+            assert np.array_equal(it, oi) and np.array_equal(conv, oc), (rate, w, early)
+            assert _post_equal(post, op), (rate, w, early)
+            hp, _, _ = _gpu(mm, llr, cfg, posteriors=False, hard_packed=True)
+            assert np.array_equal(hp, np.packbits(oh, axis=-1)), (rate, w, early)
