@@ -113,6 +113,13 @@ __device__ __forceinline__ uint32_t vmin3(uint32_t a, uint32_t b, uint32_t c) {
   asm("{\n\t.reg .b32 t;\n\tmin.s16x2 t, %1, %2;\n\tmin.s16x2 %0, t, %3;\n\t}" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
+// lane sign bit set exactly where the lane's int16 is <= 0 (the hard decision):
+// min(x - 1, x) -- add + min in one asm block so that ptxas forms VIADDMNMX
+__device__ __forceinline__ uint32_t hard_sign2(uint32_t x) {
+  uint32_t d;
+  asm("{\n\t.reg .b32 t;\n\tadd.s16x2 t, %1, %2;\n\tmin.s16x2 %0, t, %1;\n\t}" : "=r"(d) : "r"(x), "r"(0xFFFFFFFFu));
+  return d;
+}
 // lane sign masks: 0xFFFF in a lane whose bit 15 is set
 __device__ __forceinline__ uint32_t lane_signs(uint32_t x) {
   uint32_t d; asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x)); return d;
@@ -316,12 +323,13 @@ struct Layered2 {
     constexpr int E0 = S::START[T];
     uint32_t addr[D];
     addrs<E0>(a, r, b0, b1, tab, addr);
-    // hard = post <= 0 per lane: max(post, -32767) - 1 is negative exactly for
-    // post <= 0 (the max keeps -32768 from wrapping); XOR of the lane sign
-    // bits (15, 31) = the two codewords' row parities
+    // hard = post <= 0 per lane: min(post - 1, post) is negative exactly for
+    // post <= 0 (-32768 - 1 wraps to 32767, and the min then takes -32768 itself);
+    // one VIADDMNMX.  XOR of the lane sign bits (15, 31) = the two codewords' row
+    // parities
     uint32_t par = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) par ^= vadd2(vmax2(A::lds(addr[k]), 0x80018001u), 0xFFFFFFFFu);
+    for (int k = 0; k < D; ++k) par ^= hard_sign2(A::lds(addr[k]));
     return ((par >> 15) & 1u) | ((par >> 30) & 2u);
   }
 
@@ -382,7 +390,7 @@ struct Layered2 {
     constexpr int D = S::DEG[T];
     uint32_t par = 0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) par ^= vadd2(vmax2(v[k], 0x80018001u), 0xFFFFFFFFu);
+    for (int k = 0; k < D; ++k) par ^= hard_sign2(v[k]);
     return ((par >> 15) & 1u) | ((par >> 30) & 2u);
   }
   template <int T>
