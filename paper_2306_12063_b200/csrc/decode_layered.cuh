@@ -152,6 +152,27 @@ __device__ __forceinline__ void f_mul2(float a0, float a1, float b0, float b1, f
 #ifndef QCB_F32_FMUL_SIGN
 #define QCB_F32_FMUL_SIGN 0
 #endif
+// packed fused multiply-add: (a * b + c) per lane, one rounding each (FFMA2)
+__device__ __forceinline__ void f_fma2(float a0, float a1, float b0, float b1, float c0, float c1, float& r0,
+                                       float& r1) {
+  asm("{\n\t.reg .b64 x, y, w, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\tmov.b64 w, {%6, %7};\n\t"
+      "fma.rn.f32x2 z, x, y, w;\n\tmov.b64 {%0, %1}, z;\n\t}"
+      : "=f"(r0), "=f"(r1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// Sign application without the per-edge IMAD: c = copysign(ex, zz) (one LOP3),
+// post = fma(c, +-1, zz) (FFMA2: the product is exact, so this is zz +- c with
+// the one rounding of the reference's add) and the message c * +-1 (FMUL2, off
+// the store's dependency chain): 2.5 instead of 3 instructions per edge.
+// Measured per structure (round 2, tools/exp/r02_call40.sh, coded Gb/s at 65536
+// codewords, IMAD -> FFMA2): Wi-Fi 1296 R1/2 63.3 -> 64.2, R3/4 60.3 -> 61.3, Wi-Fi
+// 1944 R5/6 59.6 -> 60.4, WiMAX 2/3A 80.5 -> 81.2, 3/4A 69.7 -> 70.7, C1 43.5 ->
+// 44.1; the rest within +-0.5 % except WiMAX 1/2 (C2: 88.3 -> 85.8, spills at its
+// 128-register cap) and Wi-Fi 1944 R2/3 (57.2 -> 55.6), which keep the IMAD.
+#ifndef QCB_F32_FMA_SIGN
+#define QCB_F32_FMA_SIGN 1
+#endif
+template <class S>
+constexpr bool f32_fma_sign() { return S::ID != 12 && S::ID != 5; }
 __device__ __forceinline__ void f_add2(float a0, float a1, float b0, float b1, float& r0, float& r1) {
   asm("{\n\t.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
       "add.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;\n\t}"
@@ -277,7 +298,7 @@ struct ArithF32 {
   // `a < nm1` / `a < nm2` do) and the chains are seeded with +inf, the
   // reference's initial min1 / min2.  3*D - 6 min instructions per row
   // instead of ~2.1*D for min1/min2 plus 2*D for the per-edge min1/min2 pick.
-  template <int D>
+  template <int D, bool FMA = false>
   __device__ __forceinline__ static void row(const Val (&p)[D], Val (&o)[D], Val* msg, const RtK& K) {
     static_assert(D >= 2, "row degree >= 2");
     float zz[D];
@@ -325,6 +346,23 @@ struct ArithF32 {
     for (int k = 1; k < D - 1; ++k) ex[k] = fminf(pre[k], suf[k]);
 #endif
     // pass 2 (_kernels.py:76-79): L_new = +-ex, sign = parity ^ sign(zz_k)
+    if constexpr (FMA && QCB_F32_FMA_SIGN) {
+      const float sp = __uint_as_float(0x3F800000u | sxm);   // -1.0f for an odd row, else +1.0f
+      float cs[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        uint32_t t;
+        asm("lop3.b32 %0, %1, %2, 0x80000000, 0xF8;" : "=r"(t) : "r"(__float_as_uint(ex[k])), "r"(__float_as_uint(zz[k])));  // ex | (zz & sign)
+        cs[k] = __uint_as_float(t);
+      }
+#pragma unroll
+      for (int k = 0; k + 1 < D; k += 2) f_fma2(cs[k], cs[k + 1], sp, sp, zz[k], zz[k + 1], o[k], o[k + 1]);
+      if (D & 1) o[D - 1] = __fmaf_rn(cs[D - 1], sp, zz[D - 1]);
+#pragma unroll
+      for (int k = 0; k + 1 < D; k += 2) f_mul2(cs[k], cs[k + 1], sp, sp, msg[k], msg[k + 1]);
+      if (D & 1) msg[D - 1] = __fmul_rn(cs[D - 1], sp);
+      return;
+    }
 #if QCB_F32_FMUL_SIGN
     // copysign(ex, zz) in one LOP3 (ex >= 0), then the row parity applied to
     // two edges at once by FMUL2 with (+-1, +-1): multiplying by -1 flips the
@@ -694,11 +732,11 @@ struct Layered {
         const float4 v = lds128f(ma + 16u * q);
         m[4 * q] = v.x; m[4 * q + 1] = v.y; m[4 * q + 2] = v.z; m[4 * q + 3] = v.w;
       }
-      A::template row<D>(p, o, m, K);
+      A::template row<D, f32_fma_sign<S>()>(p, o, m, K);
 #pragma unroll
       for (int q = 0; q < D4 / 4; ++q) sts128f(ma + 16u * q, m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
     } else {
-      A::template row<D>(p, o, msg + E0, K);
+      A::template row<D, f32_fma_sign<S>()>(p, o, msg + E0, K);
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) A::sts(addr[k], o[k]);
