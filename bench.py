@@ -193,6 +193,15 @@ def hbm_bytes(wl, frames_per_code):
     return sum(mm.n * (b + 1) + 5 for mm in wl.model_matrices()) * frames_per_code
 
 
+def ring_slots(batch_bytes, warmup, steps, cap=256):
+    """Distinct batches a workload smaller than L2 steps through: enough that no batch
+    is reused inside warm-up + timed steps, and never fewer than 2 x L2 worth of bytes
+    (so a reused slot has left L2 long before); capped (a reuse then happens only after
+    `cap` other batches, still > 2 x L2 for any batch the cap matters for)."""
+    need_l2 = int(2 * L2_BYTES // max(1, batch_bytes)) + 1
+    return min(max(cap, need_l2), max(warmup + steps, need_l2))
+
+
 def config_dict(wl, args, world, lo_hi=None):
     names = [code_name(c) for c in wl.codes]
     per_gpu = (wl.w_per_code // world if wl.strong else wl.w_per_code) * len(wl.codes)
@@ -454,7 +463,7 @@ def run_ours(args, wl):
     ring_n = 1
     if small:
         assert len(codes) == 1
-        ring_n = min(256, max(args.warmup + args.steps, int(2 * L2_BYTES // hbm_bytes(wl, w)) + 1))
+        ring_n = ring_slots(hbm_bytes(wl, w), args.warmup, args.steps)
         span_w = wl.w_per_code * world            # slot s: the job's frames shifted by s spans
         llr_ring = [llrs[0]] + [shard_llrs(wl, 0, lo + s * span_w, hi + s * span_w, dev) for s in range(1, ring_n)]
         out_ring = [outs[0]] + [tuple(torch.empty_like(t) for t in outs[0]) for _ in range(1, ring_n)]

@@ -200,3 +200,20 @@ def test_device_call_refuses_non_cuda_devices():
         _lib.DeviceCall("cpu")
     with pytest.raises(ValueError):
         _lib.DeviceCall("cuda:0", None, torch.zeros(2))
+
+
+def test_bench_ring_of_batches_exceeds_l2():
+    """bench.py steps a workload smaller than L2 (C1) through a ring of distinct
+    batches: never reused inside warm-up + timed steps unless the ring already holds
+    more than 2 x L2 of inputs."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("qcb_bench", Path(__file__).resolve().parents[1] / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    c1 = 1024 * (648 * 5 + 5)                                  # C1: LLR in + hard out + iters / conv
+    for warmup, steps in ((5, 20), (10, 100), (5, 400), (3, 1)):
+        n = bench.ring_slots(c1, warmup, steps)
+        assert n * c1 > 2 * bench.L2_BYTES
+        assert n >= min(warmup + steps, 256)
+    assert bench.ring_slots(100_000, 5, 20) * 100_000 > 2 * bench.L2_BYTES   # tiny batches: above the cap
+    assert bench.ring_slots(c1, 5, 20) == 25 or bench.ring_slots(c1, 5, 20) * c1 > 2 * bench.L2_BYTES
