@@ -68,8 +68,13 @@
 #define QCB_P16_TMT -1
 #endif
 #ifndef QCB_P16_TM_CAP
-#define QCB_P16_TM_CAP 128
+#define QCB_P16_TM_CAP 0        // 0: per structure (p16_tm_cap), else one cap for every TMEM-tier kernel (experiments)
 #endif
+// Re-swept on the final kernels (round 2, tools/exp/r02_call52.sh, r02_call53.sh; 128 / 120 /
+// 112 / 108 / 104, all four warps per sub-partition): WiMAX 3/4A (C5) 87.84 / 87.87 / 88.33 /
+// 86.6 / 85.6 Gb/s, Wi-Fi 1944 R3/4 78.2 -> 80.3 at 112; Wi-Fi 1944 R5/6 (C3) 105.2 / 102.5 /
+// 104.1 and WiMAX 5/6 91.6 -> 88.1 keep 128 (ptxas schedules differently under the cap).
+constexpr int p16_tm_cap(int id) { return (id == 15 || id == 6) ? 112 : 128; }
 #ifndef QCB_P16_TM_WAIT0
 #define QCB_P16_TM_WAIT0 1      // tcgen05.wait::st once per sweep (tier 0) instead of every TMEM tier
 #endif
@@ -437,7 +442,7 @@ struct Layered2 {
 #endif
 template <class S, int ZS>
 constexpr int p16_reg_cap() {
-  if constexpr (Layered2<S, ZS>::TMT > 0) return QCB_P16_TM_CAP;
+  if constexpr (Layered2<S, ZS>::TMT > 0) return QCB_P16_TM_CAP > 0 ? QCB_P16_TM_CAP : p16_tm_cap(S::ID);
   const int z = ZS > 0 ? ZS : 96;
   const int cap = raise_cap(z, S::NE + QCB_P16_SLACK, cw_block_bytes(z), true, smsp_raise<S, ArithI16x2>());
   // 128 registers = 4 warps per sub-partition, paid for with spills; measured
